@@ -1,0 +1,123 @@
+/* nsg.h -- C-ABI of the B200 batched small-set sorter (libnsg.so).
+ *
+ * Drop-in boundary for the reference's compiled lane.  The reference binds
+ * its C core through Cython (`pkg/src/netsort/_native.pyx:18-73`, which
+ * declares `netsort_core.h:185-208`); a maintainer swaps that binding for
+ * ctypes/Cython declarations of the functions below.
+ *
+ * Conventions (kept from the reference, netsort_core.h / _native.pyx:153-160):
+ *   return 0 on success; -1 verification failure (CorrectnessFailure);
+ *   -2 spec or size rejected (UnsupportedSize / ConfigurationError);
+ *   -3 CUDA error (message in nsg_last_error()).
+ *   The caller owns every buffer.  Device entry points are stream-ordered and
+ *   asynchronous (`stream` is a cudaStream_t, NULL = legacy default stream);
+ *   they never allocate.  `*_host` entry points take HOST buffers, pipeline the
+ *   host<->device copies with the kernels and return after the results are
+ *   back in host memory.  All entry points are thread-safe and reentrant on
+ *   disjoint buffers; the caller selects the device (cudaSetDevice).
+ */
+#ifndef NSG_H
+#define NSG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NSG_OK 0
+#define NSG_ERR_CHECK (-1)
+#define NSG_ERR_SPEC (-2)
+#define NSG_ERR_CUDA (-3)
+
+/* kinds / families / tie modes: reference registry.py:24, networks.py:30 */
+enum { NSG_KIND_NETWORK = 0, NSG_KIND_INSERTION = 1, NSG_KIND_RSS = 2, NSG_KIND_HYBRID = 3, NSG_KIND_STD = 4 };
+enum { NSG_KEY_U32 = 0, NSG_KEY_U64 = 1, NSG_KEY_I32 = 2, NSG_KEY_I64 = 3, NSG_KEY_F32 = 4, NSG_KEY_F64 = 5 };
+enum { NSG_PAY_NONE = 0, NSG_PAY_U32 = 1, NSG_PAY_U64 = 2 };
+enum { NSG_TIE_REF = 0, NSG_TIE_UNIQUE = 1 };
+
+/* First 14 fields: the reference's `ns_spec` (netsort_core.h:156-171), same
+ * order (== registry.SorterSpec._fields, pinned by test_backends.py:33-41).
+ * Tail: the typed-batch extension used by nsg_sort_rows / nsg_sort_segments
+ * (ignored by the AoS entry points, which are u64 key + u64 ref, REF mode). */
+typedef struct {
+  int kind;
+  int family;
+  int swap;
+  int ins_variant;
+  int base_kind;
+  int rss_oversampling;
+  int rss_block;
+  int rss_threshold;
+  uint32_t rss_sample_seed;
+  int qs_base_is_rss;
+  int qs_threshold;
+  int qs_depth_factor;
+  int qs_final_pass;
+  int pivot_swap;
+  /* extension */
+  int key_dtype;     /* NSG_KEY_* */
+  int payload_dtype; /* NSG_PAY_* */
+  int descending;    /* 0 ascending, 1 descending (by key, then payload in UNIQUE mode) */
+  int tie_mode;      /* NSG_TIE_REF: key-only strict < (reference semantics);
+                        NSG_TIE_UNIQUE: lexicographic (key, payload) */
+} nsg_spec;
+
+/* Replaces `_native.run_sorter_many(spec, rows)` (_native.pyx:190-208), i.e.
+ * `for i in range(m): ns_run_sorter(&sp, rows + i*n, n, ...)`
+ * (netsort_core.c:498-527).  `rows` is a DEVICE pointer to m*n packed
+ * {uint64 key; uint64 ref} items (items.py:14), 16-byte aligned, sorted in
+ * place row by row.  kind NETWORK: n in 2..16 (n < 2 is a no-op, else -2);
+ * kind RSS: n <= 1024; kind INSERTION: stable by key, n <= 1024. */
+int nsg_run_sorter_many(const nsg_spec* sp, void* rows, int64_t m, int64_t n, void* stream);
+
+/* Same with HOST rows (pinned memory overlaps copies with sorting). */
+int nsg_run_sorter_many_host(const nsg_spec* sp, void* rows, int64_t m, int64_t n);
+
+/* Typed SoA batch: `rows` rows of n keys (key_dtype) and optional payloads
+ * (payload_dtype), row-major, device pointers, 16-byte aligned.  Out-of-place
+ * or in-place (out == in).  Network kinds: n 1..16.  RSS / INSERTION: n <= 1024. */
+int nsg_sort_rows(const nsg_spec* sp, const void* keys_in, void* keys_out, const void* pay_in, void* pay_out,
+                  int64_t rows, int64_t n, void* stream);
+
+/* Same with HOST buffers (H2D, sort, D2H pipelined in chunks). */
+int nsg_sort_rows_host(const nsg_spec* sp, const void* keys_in, void* keys_out, const void* pay_in,
+                       void* pay_out, int64_t rows, int64_t n);
+
+/* Segmented (CSR) batch: segment s = [offsets[s], offsets[s+1]) of keys /
+ * payloads; lengths 0..16 are sorted by the exact-length network of the spec's
+ * family; longer segments by the warp RSS sorter.  `ws` is a device workspace
+ * of nsg_segments_ws_bytes(nseg, nelem) bytes. */
+size_t nsg_segments_ws_bytes(int64_t nseg, int64_t nelem);
+int nsg_sort_segments(const nsg_spec* sp, const uint32_t* offsets, int64_t nseg, const void* keys_in,
+                      void* keys_out, const void* pay_in, void* pay_out, void* ws, size_t ws_bytes, void* stream);
+
+/* Replaces `_native.swap_pairs(code, rows)` / `ns_cswap_dyn` (netsort_core.c:106-118):
+ * one conditional swap per (left, right) pair of DEVICE items. */
+int nsg_swap_pairs(int code, void* pairs, int64_t m, void* stream);
+
+/* Replaces `ns_classify_block` (netsort_core.c:270-300): tags[i] =
+ * ((s1<k)<<1) + ((s1<k ? s2 : s0) < k) for n DEVICE u64 keys. */
+int nsg_classify_block(const uint64_t* keys, int64_t n, uint64_t s0, uint64_t s1, uint64_t s2, int block,
+                       uint8_t* tags, void* stream);
+
+/* Replaces `ns_lcg_next` (netsort_core.c:38-40) on the host. */
+uint32_t nsg_lcg_next(uint32_t seed);
+
+/* Seeded counter-based generator for synthetic batches (splitmix64 of
+ * (seed, global index)), identical on every device and in oracle/. */
+int nsg_fill_splitmix(void* out, int64_t count, int elem_bytes, uint64_t seed, uint64_t first_index,
+                      void* stream);
+
+/* Last error message of the calling thread ("" if none). */
+const char* nsg_last_error(void);
+
+/* ABI version (major*100 + minor). */
+int nsg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NSG_H */

@@ -1,0 +1,344 @@
+// extern "C" boundary of libnsg.so (declared in include/nsg.h).
+//
+// Host-side responsibilities only: validate the spec exactly like the
+// reference's Cython wrapper (_native.pyx:85-95,153-208), pick the kernel
+// instance, size the persistent grid from the measured occupancy, launch on
+// the caller's stream, and map failures to the reference's status codes.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/nsg.h"
+#include "dispatch.h"
+#include "kernels.cuh"
+#include "net_sort.cuh"
+
+namespace nsg {
+
+static thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+static int cuda_fail(cudaError_t e, const char* what) {
+  return fail(NSG_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define NSG_CUDA(call)                                  \
+  do {                                                  \
+    cudaError_t e_ = (call);                            \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+  } while (0)
+
+KernelInfo net_lookup(int n, int dag, int key_bytes, int pay, int mode, int layout) {
+  switch (n) {
+    case 1: return net_lookup_n1(dag, key_bytes, pay, mode, layout);
+    case 2: return net_lookup_n2(dag, key_bytes, pay, mode, layout);
+    case 3: return net_lookup_n3(dag, key_bytes, pay, mode, layout);
+    case 4: return net_lookup_n4(dag, key_bytes, pay, mode, layout);
+    case 5: return net_lookup_n5(dag, key_bytes, pay, mode, layout);
+    case 6: return net_lookup_n6(dag, key_bytes, pay, mode, layout);
+    case 7: return net_lookup_n7(dag, key_bytes, pay, mode, layout);
+    case 8: return net_lookup_n8(dag, key_bytes, pay, mode, layout);
+    case 9: return net_lookup_n9(dag, key_bytes, pay, mode, layout);
+    case 10: return net_lookup_n10(dag, key_bytes, pay, mode, layout);
+    case 11: return net_lookup_n11(dag, key_bytes, pay, mode, layout);
+    case 12: return net_lookup_n12(dag, key_bytes, pay, mode, layout);
+    case 13: return net_lookup_n13(dag, key_bytes, pay, mode, layout);
+    case 14: return net_lookup_n14(dag, key_bytes, pay, mode, layout);
+    case 15: return net_lookup_n15(dag, key_bytes, pay, mode, layout);
+    case 16: return net_lookup_n16(dag, key_bytes, pay, mode, layout);
+    default: return KernelInfo{};
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Launch plumbing: per-(device, kernel) smem attribute + occupancy cache.
+// ---------------------------------------------------------------------------
+struct LaunchGeom {
+  int ctas_per_sm = 0;
+  int sms = 0;
+};
+
+static std::mutex g_mu;
+static std::unordered_map<uint64_t, LaunchGeom> g_geom;
+
+static int launch_geom(const void* fn, int threads, int smem, LaunchGeom* out) {
+  int dev = 0;
+  NSG_CUDA(cudaGetDevice(&dev));
+  const uint64_t key = (uint64_t(reinterpret_cast<uintptr_t>(fn)) << 8) ^ uint64_t(dev);
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_geom.find(key);
+    if (it != g_geom.end()) {
+      *out = it->second;
+      return 0;
+    }
+  }
+  LaunchGeom g;
+  NSG_CUDA(cudaDeviceGetAttribute(&g.sms, cudaDevAttrMultiProcessorCount, dev));
+  if (smem > 48 * 1024) NSG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  NSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g.ctas_per_sm, fn, threads, smem));
+  if (g.ctas_per_sm < 1) return fail(NSG_ERR_CUDA, "kernel cannot be resident (smem %d B)", smem);
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_geom[key] = g;
+  *out = g;
+  return 0;
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+static int launch_net(const KernelInfo& k, NetParams prm, cudaStream_t stream) {
+  if (!k.fn) return fail(NSG_ERR_SPEC, "no network kernel for this configuration");
+  if (prm.rows <= 0) return 0;
+  LaunchGeom g;
+  if (int rc = launch_geom(k.fn, k.threads, k.smem, &g)) return rc;
+  const int64_t tiles = (prm.rows + k.rows_per_warp - 1) / k.rows_per_warp;
+  const int64_t ctas_needed = (tiles + k.warps - 1) / k.warps;
+  const int64_t grid = std::min<int64_t>(ctas_needed, int64_t(g.sms) * g.ctas_per_sm);
+  void* args[] = {&prm};
+  NSG_CUDA(cudaLaunchKernel(k.fn, dim3(unsigned(grid)), dim3(unsigned(k.threads)), args, size_t(k.smem), stream));
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Spec validation
+// ---------------------------------------------------------------------------
+static int key_bytes_of(int dt) {
+  switch (dt) {
+    case NSG_KEY_U32: case NSG_KEY_I32: case NSG_KEY_F32: return 4;
+    case NSG_KEY_U64: case NSG_KEY_I64: case NSG_KEY_F64: return 8;
+    default: return 0;
+  }
+}
+static int pay_bytes_of(int pt) { return pt == NSG_PAY_U32 ? 4 : pt == NSG_PAY_U64 ? 8 : 0; }
+
+Xform make_xform(const nsg_spec& sp) {
+  Xform f{};
+  const int kb = key_bytes_of(sp.key_dtype);
+  const uint64_t sign = kb == 4 ? 0x80000000ull : 0x8000000000000000ull;
+  const bool is_signed = sp.key_dtype == NSG_KEY_I32 || sp.key_dtype == NSG_KEY_I64;
+  const bool is_float = sp.key_dtype == NSG_KEY_F32 || sp.key_dtype == NSG_KEY_F64;
+  f.sign_or = (is_signed || is_float) ? sign : 0;
+  f.flt = is_float ? 1 : 0;
+  f.kdesc = sp.descending ? ~0ull : 0ull;
+  f.pdesc = (sp.descending && sp.tie_mode == NSG_TIE_UNIQUE && sp.payload_dtype != NSG_PAY_NONE) ? ~0ull : 0ull;
+  f.active = (f.sign_or | f.kdesc | f.pdesc | uint64_t(f.flt)) != 0;
+  return f;
+}
+
+static int check_common(const nsg_spec* sp) {
+  if (!sp) return fail(NSG_ERR_SPEC, "null spec");
+  if (sp->family < 0 || sp->family > 3) return fail(NSG_ERR_SPEC, "network family code %d not in 0..3", sp->family);
+  if (sp->swap < 0 || sp->swap > 8) return fail(NSG_ERR_SPEC, "swap code %d not in 0..8", sp->swap);
+  return 0;
+}
+
+static int dag_of(const nsg_spec& sp) { return sp.family == 0 ? 0 : 1; }
+
+}  // namespace nsg
+
+using namespace nsg;
+
+extern "C" {
+
+const char* nsg_last_error(void) { return g_err.c_str(); }
+int nsg_version(void) { return 100; }
+
+uint32_t nsg_lcg_next(uint32_t seed) { return uint32_t((uint64_t(seed) * 48271u) % 2147483647u); }
+
+int nsg_sort_rows(const nsg_spec* sp, const void* keys_in, void* keys_out, const void* pay_in, void* pay_out,
+                  int64_t rows, int64_t n, void* stream) {
+  g_err.clear();
+  if (int rc = check_common(sp)) return rc;
+  const int kb = key_bytes_of(sp->key_dtype);
+  if (!kb) return fail(NSG_ERR_SPEC, "unknown key dtype %d", sp->key_dtype);
+  if (sp->payload_dtype < 0 || sp->payload_dtype > 2) return fail(NSG_ERR_SPEC, "unknown payload dtype");
+  if (sp->tie_mode != NSG_TIE_REF && sp->tie_mode != NSG_TIE_UNIQUE) return fail(NSG_ERR_SPEC, "bad tie mode");
+  if (rows < 0 || n < 0) return fail(NSG_ERR_SPEC, "negative shape");
+  const bool has_p = sp->payload_dtype != NSG_PAY_NONE;
+  if (!aligned16(keys_in) || !aligned16(keys_out) || (has_p && (!aligned16(pay_in) || !aligned16(pay_out))))
+    return fail(NSG_ERR_SPEC, "device buffers must be 16-byte aligned");
+  if (rows == 0 || n == 0) return 0;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (sp->kind == NSG_KIND_NETWORK) {
+    if (n > 16) return fail(NSG_ERR_SPEC, "network sorters cover 2..16 items, got %lld", (long long)n);
+    NetParams prm{keys_in, keys_out, pay_in, pay_out, rows, make_xform(*sp)};
+    const KernelInfo k = net_lookup(int(n), dag_of(*sp), kb, sp->payload_dtype, sp->tie_mode, LAYOUT_SOA);
+    return launch_net(k, prm, st);
+  }
+  if (sp->kind == NSG_KIND_RSS || sp->kind == NSG_KIND_INSERTION)
+    return launch_rss_rows(*sp, keys_in, keys_out, pay_in, pay_out, rows, n, st);
+  return fail(NSG_ERR_SPEC, "sorter kind %d is not a batched small-set sorter (out of scope)", sp->kind);
+}
+
+int nsg_run_sorter_many(const nsg_spec* sp, void* rows, int64_t m, int64_t n, void* stream) {
+  g_err.clear();
+  if (int rc = check_common(sp)) return rc;
+  if (m < 0 || n < 0) return fail(NSG_ERR_SPEC, "negative shape");
+  if (!aligned16(rows)) return fail(NSG_ERR_SPEC, "item rows must be 16-byte aligned");
+  if (m == 0 || n == 0) return 0;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (sp->kind == NSG_KIND_NETWORK) {
+    if (n < 2) return 0;  // ns_run_sorter: n < 2 -> 0 (netsort_core.c:502-503)
+    if (n > 16) return fail(NSG_ERR_SPEC, "network sorters cover 2..16 items, got %lld", (long long)n);
+    NetParams prm{rows, rows, nullptr, nullptr, m, Xform{}};
+    return launch_net(net_lookup(int(n), dag_of(*sp), 8, 2, MODE_REF, LAYOUT_AOS16), prm, st);
+  }
+  if (sp->kind == NSG_KIND_RSS || sp->kind == NSG_KIND_INSERTION) return launch_rss_items(*sp, rows, m, n, st);
+  return fail(NSG_ERR_SPEC, "sorter kind %d is not a batched small-set sorter (out of scope)", sp->kind);
+}
+
+// ---------------------------------------------------------------------------
+// Host-buffer entry points: chunked H2D -> sort -> D2H on two streams, so the
+// copy engines and the SMs overlap.  Device staging buffers are cached per
+// device and only grow.
+// ---------------------------------------------------------------------------
+struct HostPipe {
+  cudaStream_t s[2] = {nullptr, nullptr};
+  void* buf[2] = {nullptr, nullptr};
+  size_t cap = 0;
+};
+static std::mutex g_pipe_mu;
+static std::unordered_map<int, HostPipe> g_pipes;
+
+static int get_pipe(size_t bytes_per_buf, HostPipe** out) {
+  int dev = 0;
+  NSG_CUDA(cudaGetDevice(&dev));
+  HostPipe& p = g_pipes[dev];
+  if (!p.s[0]) {
+    NSG_CUDA(cudaStreamCreateWithFlags(&p.s[0], cudaStreamNonBlocking));
+    NSG_CUDA(cudaStreamCreateWithFlags(&p.s[1], cudaStreamNonBlocking));
+  }
+  if (p.cap < bytes_per_buf) {
+    for (int i = 0; i < 2; ++i) {
+      if (p.buf[i]) NSG_CUDA(cudaFree(p.buf[i]));
+      p.buf[i] = nullptr;
+    }
+    p.cap = 0;
+    for (int i = 0; i < 2; ++i) NSG_CUDA(cudaMalloc(&p.buf[i], bytes_per_buf));
+    p.cap = bytes_per_buf;
+  }
+  *out = &p;
+  return 0;
+}
+
+static constexpr size_t kChunkBytes = size_t(64) << 20;
+
+int nsg_sort_rows_host(const nsg_spec* sp, const void* keys_in, void* keys_out, const void* pay_in,
+                       void* pay_out, int64_t rows, int64_t n) {
+  g_err.clear();
+  if (int rc = check_common(sp)) return rc;
+  const int kb = key_bytes_of(sp->key_dtype);
+  if (!kb) return fail(NSG_ERR_SPEC, "unknown key dtype %d", sp->key_dtype);
+  if (rows <= 0 || n <= 0) return 0;
+  const int pb = pay_bytes_of(sp->payload_dtype);
+  const size_t row_k = size_t(n) * kb, row_p = size_t(n) * pb;
+  // chunk rows so that each chunk is ~64 MiB and a multiple of 16 bytes per region
+  int64_t crow = std::max<int64_t>(1, int64_t(kChunkBytes / (row_k + row_p)));
+  crow = (crow + 15) / 16 * 16;
+  crow = std::min<int64_t>(crow, rows);
+  const size_t kbytes_c = (size_t(crow) * row_k + 15) / 16 * 16;
+  const size_t pbytes_c = (size_t(crow) * row_p + 15) / 16 * 16;
+  std::lock_guard<std::mutex> lk(g_pipe_mu);
+  HostPipe* p = nullptr;
+  if (int rc = get_pipe(kbytes_c + pbytes_c, &p)) return rc;
+  const char* ki = static_cast<const char*>(keys_in);
+  char* ko = static_cast<char*>(keys_out);
+  const char* pi = static_cast<const char*>(pay_in);
+  char* po = static_cast<char*>(pay_out);
+  int64_t c = 0;
+  for (int64_t r0 = 0; r0 < rows; r0 += crow, ++c) {
+    const int64_t rr = std::min<int64_t>(crow, rows - r0);
+    cudaStream_t s = p->s[c & 1];
+    char* dk = static_cast<char*>(p->buf[c & 1]);
+    char* dp = dk + kbytes_c;
+    NSG_CUDA(cudaMemcpyAsync(dk, ki + size_t(r0) * row_k, size_t(rr) * row_k, cudaMemcpyHostToDevice, s));
+    if (pb) NSG_CUDA(cudaMemcpyAsync(dp, pi + size_t(r0) * row_p, size_t(rr) * row_p, cudaMemcpyHostToDevice, s));
+    if (int rc = nsg_sort_rows(sp, dk, dk, pb ? dp : nullptr, pb ? dp : nullptr, rr, n, s)) return rc;
+    NSG_CUDA(cudaMemcpyAsync(ko + size_t(r0) * row_k, dk, size_t(rr) * row_k, cudaMemcpyDeviceToHost, s));
+    if (pb) NSG_CUDA(cudaMemcpyAsync(po + size_t(r0) * row_p, dp, size_t(rr) * row_p, cudaMemcpyDeviceToHost, s));
+  }
+  NSG_CUDA(cudaStreamSynchronize(p->s[0]));
+  NSG_CUDA(cudaStreamSynchronize(p->s[1]));
+  return 0;
+}
+
+int nsg_run_sorter_many_host(const nsg_spec* sp, void* rows, int64_t m, int64_t n) {
+  g_err.clear();
+  if (int rc = check_common(sp)) return rc;
+  if (m <= 0 || n <= 0) return 0;
+  if (sp->kind == NSG_KIND_NETWORK && n < 2) return 0;
+  if (sp->kind == NSG_KIND_NETWORK && n > 16) return fail(NSG_ERR_SPEC, "network sorters cover 2..16 items");
+  const size_t row_b = size_t(n) * 16;
+  int64_t crow = std::max<int64_t>(1, int64_t(kChunkBytes / row_b));
+  crow = std::min<int64_t>(crow, m);
+  std::lock_guard<std::mutex> lk(g_pipe_mu);
+  HostPipe* p = nullptr;
+  if (int rc = get_pipe(size_t(crow) * row_b, &p)) return rc;
+  char* h = static_cast<char*>(rows);
+  int64_t c = 0;
+  for (int64_t r0 = 0; r0 < m; r0 += crow, ++c) {
+    const int64_t rr = std::min<int64_t>(crow, m - r0);
+    cudaStream_t s = p->s[c & 1];
+    char* d = static_cast<char*>(p->buf[c & 1]);
+    NSG_CUDA(cudaMemcpyAsync(d, h + size_t(r0) * row_b, size_t(rr) * row_b, cudaMemcpyHostToDevice, s));
+    if (int rc = nsg_run_sorter_many(sp, d, rr, n, s)) return rc;
+    NSG_CUDA(cudaMemcpyAsync(h + size_t(r0) * row_b, d, size_t(rr) * row_b, cudaMemcpyDeviceToHost, s));
+  }
+  NSG_CUDA(cudaStreamSynchronize(p->s[0]));
+  NSG_CUDA(cudaStreamSynchronize(p->s[1]));
+  return 0;
+}
+
+int nsg_swap_pairs(int code, void* pairs, int64_t m, void* stream) {
+  g_err.clear();
+  if (code < 0 || code > 8) return fail(NSG_ERR_SPEC, "swap code %d not in 0..8", code);
+  if (m <= 0) return 0;
+  if (!aligned16(pairs)) return fail(NSG_ERR_SPEC, "pairs must be 16-byte aligned");
+  return launch_swap_pairs(pairs, m, static_cast<cudaStream_t>(stream));
+}
+
+int nsg_classify_block(const uint64_t* keys, int64_t n, uint64_t s0, uint64_t s1, uint64_t s2, int block,
+                       uint8_t* tags, void* stream) {
+  g_err.clear();
+  if (n <= 0) return 0;
+  (void)block;  // block interleaving is a CPU ILP device; results are per element
+  return launch_classify(keys, n, s0, s1, s2, tags, static_cast<cudaStream_t>(stream));
+}
+
+int nsg_fill_splitmix(void* out, int64_t count, int elem_bytes, uint64_t seed, uint64_t first_index,
+                      void* stream) {
+  g_err.clear();
+  if (elem_bytes != 4 && elem_bytes != 8) return fail(NSG_ERR_SPEC, "elem_bytes must be 4 or 8");
+  if (count <= 0) return 0;
+  return launch_fill_splitmix(out, count, elem_bytes, seed, first_index, static_cast<cudaStream_t>(stream));
+}
+
+size_t nsg_segments_ws_bytes(int64_t nseg, int64_t nelem) { return segments_ws_bytes(nseg, nelem); }
+
+int nsg_sort_segments(const nsg_spec* sp, const uint32_t* offsets, int64_t nseg, const void* keys_in,
+                      void* keys_out, const void* pay_in, void* pay_out, void* ws, size_t ws_bytes, void* stream) {
+  g_err.clear();
+  if (int rc = check_common(sp)) return rc;
+  if (!key_bytes_of(sp->key_dtype)) return fail(NSG_ERR_SPEC, "unknown key dtype %d", sp->key_dtype);
+  if (nseg <= 0) return 0;
+  return launch_segments(*sp, offsets, nseg, keys_in, keys_out, pay_in, pay_out, ws, ws_bytes,
+                         static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

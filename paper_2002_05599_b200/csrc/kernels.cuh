@@ -1,0 +1,32 @@
+// Host-side launchers implemented in the other translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/nsg.h"
+#include "common.cuh"
+
+namespace nsg {
+
+int fail(int code, const char* fmt, ...);
+Xform make_xform(const nsg_spec& sp);
+
+// misc.cu
+int launch_swap_pairs(void* pairs, int64_t m, cudaStream_t st);
+int launch_classify(const uint64_t* keys, int64_t n, uint64_t s0, uint64_t s1, uint64_t s2, uint8_t* tags,
+                    cudaStream_t st);
+int launch_fill_splitmix(void* out, int64_t count, int elem_bytes, uint64_t seed, uint64_t first, cudaStream_t st);
+
+// rss.cu
+int launch_rss_rows(const nsg_spec& sp, const void* keys_in, void* keys_out, const void* pay_in, void* pay_out,
+                    int64_t rows, int64_t n, cudaStream_t st);
+int launch_rss_items(const nsg_spec& sp, void* rows, int64_t m, int64_t n, cudaStream_t st);
+
+// segments.cu
+size_t segments_ws_bytes(int64_t nseg, int64_t nelem);
+int launch_segments(const nsg_spec& sp, const uint32_t* offsets, int64_t nseg, const void* keys_in, void* keys_out,
+                    const void* pay_in, void* pay_out, void* ws, size_t ws_bytes, cudaStream_t st);
+
+}  // namespace nsg

@@ -1,0 +1,314 @@
+// Fixed-width batched network sort: B independent rows of N items each.
+//
+// Replaces the reference hot loop `_native.run_sorter_many` (_native.pyx:190-208)
+// -> `ns_run_sorter` kind 0 (netsort_core.c:498-509) -> one generated
+// straight-line network per row (gen/netsort_nets_*.c).  Design:
+//
+//  * one WARP owns a tile of ROWS = 32*APL consecutive rows; tiles are
+//    distributed grid-stride over a persistent grid, so there is no CTA-wide
+//    barrier anywhere -- only __syncwarp;
+//  * the tile's bytes are copied HBM -> shared memory by cp.async (16-byte
+//    LDGSTS, L2-only) into a STAGES-deep per-warp ring, so the loads of tiles
+//    i+1..i+STAGES-1 are in flight while tile i is sorted;
+//  * rows are laid out in shared memory with a stride that is an ODD multiple
+//    of the per-lane vector width (pad 16 B when the row is an even number of
+//    16-byte chunks) -> every lane reads/writes its own row with conflict-free
+//    LDS.128/.64/.32;
+//  * each lane sorts its row in registers with the unrolled network of
+//    csrc/gen/nets.cuh, writes it back in place, and the warp streams the tile
+//    out with coalesced 16-byte stores.
+//
+// Layouts: SoA (separate key[] and payload[] arrays) or AoS16 (the reference's
+// packed {u64 key, u64 ref} item, items.py:14).
+#pragma once
+
+#include "common.cuh"
+#include "gen/nets.cuh"
+
+namespace nsg {
+
+enum Mode { MODE_REF = 0, MODE_UNIQUE = 1 };
+enum Layout { LAYOUT_SOA = 0, LAYOUT_AOS16 = 1 };
+
+struct NetParams {
+  const void* k_in;
+  void* k_out;
+  const void* p_in;
+  void* p_out;
+  int64_t rows;
+  Xform xf;
+};
+
+// Shared-memory geometry of one region (keys, payloads, or AoS items).
+template <int N, int EB>
+struct RowGeom {
+  static constexpr int R = N * EB;  // row bytes in HBM
+  static constexpr int V = (R % 16 == 0) ? 16 : ((R % 8 == 0) ? 8 : 4);
+  static constexpr bool PAD = (V == 16) && ((R / 16) % 2 == 0);
+  static constexpr int RS = R + (PAD ? 16 : 0);  // row stride in smem
+  static constexpr int W = R / 4;                // 32-bit words per row
+
+  // smem byte offset of the 16-byte chunk q of the contiguous tile
+  __device__ __forceinline__ static int chunk_off(int q) {
+    if constexpr (PAD) {
+      constexpr int C = R / 16;
+      return (q / C) * RS + (q % C) * 16;
+    } else {
+      return q * 16;
+    }
+  }
+
+  __device__ __forceinline__ static void load_row(const unsigned char* base, int r, uint32_t (&w)[W]) {
+    const unsigned char* rp = base + r * RS;
+#pragma unroll
+    for (int i = 0; i < R / V; ++i) {
+      if constexpr (V == 16) {
+        const uint4 x = *reinterpret_cast<const uint4*>(rp + 16 * i);
+        w[4 * i] = x.x; w[4 * i + 1] = x.y; w[4 * i + 2] = x.z; w[4 * i + 3] = x.w;
+      } else if constexpr (V == 8) {
+        const uint2 x = *reinterpret_cast<const uint2*>(rp + 8 * i);
+        w[2 * i] = x.x; w[2 * i + 1] = x.y;
+      } else {
+        w[i] = *reinterpret_cast<const uint32_t*>(rp + 4 * i);
+      }
+    }
+  }
+
+  __device__ __forceinline__ static void store_row(unsigned char* base, int r, const uint32_t (&w)[W]) {
+    unsigned char* rp = base + r * RS;
+#pragma unroll
+    for (int i = 0; i < R / V; ++i) {
+      if constexpr (V == 16) {
+        *reinterpret_cast<uint4*>(rp + 16 * i) = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+      } else if constexpr (V == 8) {
+        *reinterpret_cast<uint2*>(rp + 8 * i) = make_uint2(w[2 * i], w[2 * i + 1]);
+      } else {
+        *reinterpret_cast<uint32_t*>(rp + 4 * i) = w[i];
+      }
+    }
+  }
+};
+
+template <class T>
+__device__ __forceinline__ T word_get(const uint32_t* w, int j);
+template <>
+__device__ __forceinline__ uint32_t word_get<uint32_t>(const uint32_t* w, int j) { return w[j]; }
+template <>
+__device__ __forceinline__ uint64_t word_get<uint64_t>(const uint32_t* w, int j) {
+  return uint64_t(w[2 * j]) | (uint64_t(w[2 * j + 1]) << 32);
+}
+__device__ __forceinline__ void word_put(uint32_t* w, int j, uint32_t v) { w[j] = v; }
+__device__ __forceinline__ void word_put(uint32_t* w, int j, uint64_t v) {
+  w[2 * j] = uint32_t(v);
+  w[2 * j + 1] = uint32_t(v >> 32);
+}
+
+// Compile-time configuration of one kernel instance.
+template <int N_, int DAG_, class U_, class P_, int MODE_, int LAYOUT_>
+struct NetCfg {
+  static constexpr int N = N_;
+  static constexpr int DAG = DAG_;
+  using U = U_;
+  using P = P_;
+  static constexpr bool HAS_P = !IsNoPay<P>::value;
+  static constexpr int MODE = HAS_P ? MODE_ : MODE_UNIQUE;
+  static constexpr int LAYOUT = LAYOUT_;
+  static_assert(LAYOUT != LAYOUT_AOS16 || (sizeof(U) == 8 && PayBytes<P>::value == 8), "AoS16 is u64+u64");
+  // regions: K (keys or AoS items), P (payloads, SoA only)
+  static constexpr int KEB = (LAYOUT == LAYOUT_AOS16) ? 16 : int(sizeof(U));
+  static constexpr int PEB = (LAYOUT == LAYOUT_AOS16) ? 0 : PayBytes<P>::value;
+  using GK = RowGeom<N, KEB>;
+  using GP = RowGeom<N, (PEB ? PEB : 4)>;
+  static constexpr int ROW_BYTES = GK::R + (PEB ? GP::R : 0);
+  // ~4 KiB of HBM bytes per warp per stage
+  static constexpr int APL_RAW = 4096 / (32 * ROW_BYTES);
+  static constexpr int APL = APL_RAW >= 16 ? 16 : APL_RAW >= 8 ? 8 : APL_RAW >= 4 ? 4 : APL_RAW >= 2 ? 2 : 1;
+  static constexpr int ROWS = 32 * APL;
+  static constexpr int STAGES = 3;
+  static constexpr int K_SMEM = ROWS * GK::RS;
+  static constexpr int P_SMEM = PEB ? ROWS * GP::RS : 0;
+  static constexpr int STAGE_SMEM = K_SMEM + P_SMEM;
+  static constexpr int WARPS = 4;
+  static constexpr int WARP_SMEM = STAGES * STAGE_SMEM;
+  static constexpr int CTA_SMEM = WARPS * WARP_SMEM;
+  using CX = typename std::conditional<!HAS_P, CxKeys,
+                                       typename std::conditional<MODE == MODE_REF, CxRef, CxUnique>::type>::type;
+};
+
+// ---- tile copy-in (one region) --------------------------------------------
+// Full tiles take the unrolled fast path (no per-chunk bounds); only the last
+// (partial) tile of a launch pays for byte-exact src sizes.
+template <class G, int ROWS>
+__device__ __forceinline__ void issue_region(unsigned char* sm, const unsigned char* g, int valid_bytes,
+                                             int lane) {
+  constexpr int CHUNKS = ROWS * G::R / 16;
+  if (valid_bytes == CHUNKS * 16) {
+    if constexpr (CHUNKS % 32 == 0) {
+#pragma unroll
+      for (int i = 0; i < CHUNKS / 32; ++i) {
+        const int q = i * 32 + lane;
+        cp_async16(sm + G::chunk_off(q), g + q * 16, 16);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < (CHUNKS + 31) / 32; ++i) {
+        const int q = i * 32 + lane;
+        if (q < CHUNKS) cp_async16(sm + G::chunk_off(q), g + q * 16, 16);
+      }
+    }
+  } else {
+    for (int q = lane; q < CHUNKS; q += 32) {
+      const int rem = valid_bytes - q * 16;
+      const int src = rem >= 16 ? 16 : (rem > 0 ? rem : 0);
+      cp_async16(sm + G::chunk_off(q), src ? (g + q * 16) : g, src);
+    }
+  }
+}
+
+// ---- tile copy-out (one region) -------------------------------------------
+template <class G, int ROWS>
+__device__ __forceinline__ void store_region(const unsigned char* sm, unsigned char* g, int valid_bytes,
+                                             int lane) {
+  constexpr int CHUNKS = ROWS * G::R / 16;
+  if (valid_bytes == CHUNKS * 16) {
+#pragma unroll
+    for (int i = 0; i < (CHUNKS + 31) / 32; ++i) {
+      const int q = i * 32 + lane;
+      if (CHUNKS % 32 == 0 || q < CHUNKS) {
+        const uint4 v = *reinterpret_cast<const uint4*>(sm + G::chunk_off(q));
+        stg128_cs(g + q * 16, v);
+      }
+    }
+  } else {  // tail tile: element-precise (4-byte) stores, never past the end
+    for (int q = lane; q < CHUNKS; q += 32) {
+      const int off = q * 16;
+      if (off >= valid_bytes) break;
+      const uint32_t* s = reinterpret_cast<const uint32_t*>(sm + G::chunk_off(q));
+      uint32_t* d = reinterpret_cast<uint32_t*>(g + off);
+      const int words = valid_bytes - off >= 16 ? 4 : (valid_bytes - off) / 4;
+      for (int w = 0; w < words; ++w) d[w] = s[w];
+    }
+  }
+}
+
+// ---- per-lane row sort ----------------------------------------------------
+template <class Cfg>
+__device__ __forceinline__ void sort_row(unsigned char* smk, unsigned char* smp, int r, const Xform& xf) {
+  using U = typename Cfg::U;
+  using P = typename Cfg::P;
+  using E = Elem<U, P>;
+  constexpr int N = Cfg::N;
+  E e[N];
+  uint32_t wk[Cfg::GK::W];
+  Cfg::GK::load_row(smk, r, wk);
+  if constexpr (Cfg::LAYOUT == LAYOUT_AOS16) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      e[j].k = word_get<uint64_t>(wk, 2 * j);
+      e[j].p = word_get<uint64_t>(wk, 2 * j + 1);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < N; ++j) e[j].k = word_get<U>(wk, j);
+    if constexpr (Cfg::HAS_P) {
+      uint32_t wp[Cfg::GP::W];
+      Cfg::GP::load_row(smp, r, wp);
+#pragma unroll
+      for (int j = 0; j < N; ++j) e[j].p = word_get<P>(wp, j);
+    }
+  }
+  if (xf.active) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      e[j].k = to_ord<U>(e[j].k, xf);
+      if constexpr (Cfg::HAS_P) e[j].p ^= P(xf.pdesc);
+    }
+  }
+  Net<Cfg::DAG, N>::template run<typename Cfg::CX>(e);
+  if (xf.active) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      e[j].k = from_ord<U>(e[j].k, xf);
+      if constexpr (Cfg::HAS_P) e[j].p ^= P(xf.pdesc);
+    }
+  }
+  if constexpr (Cfg::LAYOUT == LAYOUT_AOS16) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      word_put(wk, 2 * j, e[j].k);
+      word_put(wk, 2 * j + 1, e[j].p);
+    }
+    Cfg::GK::store_row(smk, r, wk);
+  } else {
+#pragma unroll
+    for (int j = 0; j < N; ++j) word_put(wk, j, e[j].k);
+    Cfg::GK::store_row(smk, r, wk);
+    if constexpr (Cfg::HAS_P) {
+      uint32_t wp[Cfg::GP::W];
+#pragma unroll
+      for (int j = 0; j < N; ++j) word_put(wp, j, e[j].p);
+      Cfg::GP::store_row(smp, r, wp);
+    }
+  }
+}
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::WARPS * 32) net_sort_kernel(const NetParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  unsigned char* wsm = smem_raw + warp * Cfg::WARP_SMEM;
+  constexpr int ROWS = Cfg::ROWS;
+  constexpr int S = Cfg::STAGES;
+  const int64_t ntiles = (p.rows + ROWS - 1) / ROWS;
+  const int64_t first = int64_t(blockIdx.x) * Cfg::WARPS + warp;
+  const int64_t stride = int64_t(gridDim.x) * Cfg::WARPS;
+  const unsigned char* kin = static_cast<const unsigned char*>(p.k_in);
+  const unsigned char* pin = static_cast<const unsigned char*>(p.p_in);
+  unsigned char* kout = static_cast<unsigned char*>(p.k_out);
+  unsigned char* pout = static_cast<unsigned char*>(p.p_out);
+
+  auto issue = [&](int64_t t, int stage) {
+    unsigned char* st = wsm + stage * Cfg::STAGE_SMEM;
+    const int64_t row0 = t * ROWS;
+    const int64_t vrows = p.rows - row0 < ROWS ? p.rows - row0 : ROWS;
+    const int vr = int(vrows);
+    issue_region<typename Cfg::GK, ROWS>(st, kin + row0 * Cfg::GK::R, vr * Cfg::GK::R, lane);
+    if constexpr (Cfg::PEB != 0)
+      issue_region<typename Cfg::GP, ROWS>(st + Cfg::K_SMEM, pin + row0 * Cfg::GP::R, vr * Cfg::GP::R, lane);
+  };
+
+#pragma unroll
+  for (int s = 0; s < S - 1; ++s) {
+    const int64_t t = first + s * stride;
+    if (t < ntiles) issue(t, s);
+    cp_async_commit();
+  }
+  int stage = 0;
+  for (int64_t t = first; t < ntiles; t += stride) {
+    const int64_t tn = t + (S - 1) * stride;
+    if (tn < ntiles) issue(tn, (stage + S - 1) % S);
+    cp_async_commit();
+    cp_async_wait<S - 1>();
+    __syncwarp();
+
+    unsigned char* smk = wsm + stage * Cfg::STAGE_SMEM;
+    unsigned char* smp = smk + Cfg::K_SMEM;
+    const int64_t row0 = t * ROWS;
+    const int vrows = p.rows - row0 < ROWS ? int(p.rows - row0) : ROWS;
+#pragma unroll
+    for (int a = 0; a < Cfg::APL; ++a) {
+      const int r = a * 32 + lane;
+      if (r < vrows) sort_row<Cfg>(smk, smp, r, p.xf);
+    }
+    __syncwarp();
+    store_region<typename Cfg::GK, ROWS>(smk, kout + row0 * Cfg::GK::R, vrows * Cfg::GK::R, lane);
+    if constexpr (Cfg::PEB != 0)
+      store_region<typename Cfg::GP, ROWS>(smp, pout + row0 * Cfg::GP::R, vrows * Cfg::GP::R, lane);
+    __syncwarp();
+    stage = (stage + 1) % S;
+  }
+  cp_async_wait<0>();
+}
+
+}  // namespace nsg

@@ -1,0 +1,285 @@
+"""GPU parity of the network path, through the C-ABI, against the oracle.
+
+Bar: bit-exact.  REF mode (key-only strict <, the reference's compare) must
+reproduce the reference's exact comparator DAG, observable through the
+payload under key ties; UNIQUE mode must equal the lexicographic
+(key, payload) sort.  Reference tests mirrored: test_acceptance.py A04/A05,
+test_smallsort.py, test_backends.py:145-203.
+"""
+
+import itertools
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+G = Path(__file__).parent / "golden"
+FAMS = ("best", "bn-l", "bn-p", "bn-r")
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+    assert t.cuda.is_available()
+    return t
+
+
+def _items(keys, refs):
+    a = np.empty(keys.shape, dtype=oracle.ITEM)
+    a["key"], a["ref"] = keys, refs
+    return a
+
+
+# ---------------------------------------------------------------------------
+# the reference's own outputs (golden) through the reference-shaped API
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("family", FAMS)
+def test_run_sorter_many_matches_reference_golden(family, torch):
+    from paper_2002_05599_b200 import backend, registry
+    net = np.load(G / "net_rows.npz")
+    spec = registry.spec_network(family, "4CmS")
+    for n in range(2, 17):
+        for kind in ("u64", "dup"):
+            t = f"{family}_{n}_{kind}"
+            rows = _items(net[f"in_key_{t}"], net[f"in_ref_{t}"])
+            backend.run_sorter_many(spec, rows)               # host buffers
+            assert np.array_equal(rows["key"], net[f"out_key_{t}"]), t
+            assert np.array_equal(rows["ref"], net[f"out_ref_{t}"]), t
+            dev = torch.from_numpy(_items(net[f"in_key_{t}"], net[f"in_ref_{t}"]).view(np.uint64)
+                                   .reshape(-1, n, 2).astype(np.int64)).cuda()
+            backend.run_sorter_many(spec, dev)                # device buffers
+            got = dev.cpu().numpy().view(np.uint64)
+            assert np.array_equal(got[:, :, 0], net[f"out_key_{t}"]), t
+            assert np.array_equal(got[:, :, 1], net[f"out_ref_{t}"]), t
+
+
+@pytest.mark.parametrize("family", FAMS)
+def test_a05_all_permutations_n8(family, torch):
+    from paper_2002_05599_b200 import backend, registry
+    perms = np.array(list(itertools.permutations(range(8))), dtype=np.uint64)
+    rows = _items(perms, perms ^ np.uint64(0xA5A5))
+    backend.run_sorter_many(registry.spec_network(family, "4CmS"), rows)
+    assert np.array_equal(rows["key"], np.sort(perms, axis=1))
+    assert np.array_equal(rows["ref"], rows["key"] ^ np.uint64(0xA5A5))
+
+
+@pytest.mark.parametrize("family", FAMS)
+def test_random_rows_every_swap_and_n_vs_reference_binary(family, torch):
+    from paper_2002_05599_b200 import backend, registry
+    from paper_2002_05599_b200.swaps import STRATEGIES
+    rng = np.random.default_rng(5)
+    for code, swap in enumerate(STRATEGIES):
+        spec = registry.spec_network(family, swap)
+        for n in range(2, 17):
+            keys = rng.integers(0, 2**64 if code % 2 else 3, size=(667, n), dtype=np.uint64)
+            refs = rng.integers(0, 2**64, size=(667, n), dtype=np.uint64)
+            rows = _items(keys, refs)
+            exp = _items(keys, refs)
+            oracle.run_items(exp, kind="network", family=family)
+            backend.run_sorter_many(spec, rows)
+            assert np.array_equal(rows, exp), (family, swap, n)
+
+
+def test_zero_one_items_with_ref_transport(torch):
+    from paper_2002_05599_b200 import smallsort
+    from paper_2002_05599_b200.items import items_from_pairs
+    for family in FAMS:
+        for n in range(2, 11):
+            allrows = np.array([[(b >> i) & 1 for i in range(n)] for b in range(1 << n)], dtype=np.uint64)
+            for bits_row in allrows[:: max(1, len(allrows) // 64)]:
+                arr = items_from_pairs(list(zip(bits_row.tolist(), range(n))))
+                smallsort.sort_network(arr, n, family, "2CPp")
+                assert arr["key"].tolist() == sorted(bits_row.tolist())
+                for k, r in zip(arr["key"].tolist(), arr["ref"].tolist()):
+                    assert bits_row[r] == k
+
+
+def test_sort_network_api_contracts(torch):
+    from paper_2002_05599_b200 import smallsort
+    from paper_2002_05599_b200.errors import UnsupportedSize
+    from paper_2002_05599_b200.items import items_from_keys, items_from_pairs
+    arr = items_from_pairs([(9, 0xA), (1, 0xB)])
+    smallsort.sort_network(arr, 2, "best", "ISwp")
+    assert arr["key"].tolist() == [1, 9] and arr["ref"].tolist() == [0xB, 0xA]
+    arr = items_from_keys([5, 4, 3, 2, 1, 0])
+    smallsort.sort_network(arr, 4, "bn-l", "TCOp")
+    assert arr["key"].tolist() == [2, 3, 4, 5, 1, 0]
+    with pytest.raises(UnsupportedSize):
+        smallsort.sort_network(items_from_keys(range(20)), 17, "best", "ISwp")
+    with pytest.raises(UnsupportedSize):
+        smallsort.sort_network(items_from_keys([3, 1]), 3, "best", "ISwp")
+    arr = items_from_pairs([(7, i) for i in range(8)])
+    smallsort.sort_network(arr, 8, "best", "6Cm")
+    assert arr["key"].tolist() == [7] * 8 and arr["ref"].tolist() == list(range(8))  # equal keys never swap
+
+
+def test_swap_pairs_a04(torch):
+    from paper_2002_05599_b200 import backend
+    rng = np.random.default_rng(4)
+    pairs = np.empty((100_000, 2), dtype=oracle.ITEM)
+    pairs["key"] = rng.integers(0, 2**64, size=(100_000, 2), dtype=np.uint64)
+    pairs["ref"] = rng.integers(0, 2**64, size=(100_000, 2), dtype=np.uint64)
+    pairs["key"][::10, 1] = pairs["key"][::10, 0]
+    expected = pairs.copy()
+    m = pairs["key"][:, 1] < pairs["key"][:, 0]
+    expected[m] = expected[m][:, ::-1]
+    for code in range(9):
+        got = pairs.copy()
+        backend.swap_pairs(code, got)
+        assert np.array_equal(got, expected), code
+
+
+def test_classify_matches_reference_golden(torch):
+    from paper_2002_05599_b200 import rss
+    c = np.load(G / "classify.npz")
+    for block in range(1, 6):
+        s = c[f"spl_{block}"]
+        got = rss.classify_block(c[f"keys_{block}"], rss.SplitterSet(*map(int, s)), block)
+        assert np.array_equal(got, c[f"tags_{block}"])
+    assert rss.classify_block(np.array([5, 15, 25, 35], dtype=np.uint64),
+                              rss.SplitterSet(10, 20, 30), 4).tolist() == [0, 1, 2, 3]
+
+
+# ---------------------------------------------------------------------------
+# typed SoA batches vs the oracle (every n, dtype, payload, mode, direction)
+# ---------------------------------------------------------------------------
+
+KEY_DTYPES = ["uint32", "uint64", "int32", "int64", "float32", "float64"]
+
+
+def _keys(rng, dtype, shape, dup):
+    if dtype.startswith("float"):
+        x = rng.standard_normal(shape).astype(dtype)
+        if dup:
+            x = np.round(x * 2).astype(dtype)
+        return x
+    info = np.iinfo(dtype)
+    if dup:
+        return rng.integers(0, 3, size=shape).astype(dtype)
+    return rng.integers(info.min, info.max, size=shape, dtype=dtype, endpoint=True)
+
+
+@pytest.mark.parametrize("kdt", KEY_DTYPES)
+@pytest.mark.parametrize("pdt", [None, "uint32", "uint64"])
+def test_sort_rows_typed_vs_oracle(kdt, pdt, torch):
+    from paper_2002_05599_b200 import batch
+    rng = np.random.default_rng(abs(hash((kdt, pdt))) % 2**32)
+    rows = 1000 + 37  # ragged tail tile
+    for n in range(1, 17):
+        for family in ("best", "bn-l"):
+            modes = ["unique"] if pdt is None else ["unique", "ref"]
+            for tie in modes:
+                for desc in (False, True):
+                    dup = (n + desc) % 2 == 0
+                    keys = _keys(rng, kdt, (rows, n), dup)
+                    pay = None if pdt is None else rng.integers(0, 2**31, size=(rows, n)).astype(pdt)
+                    ek, ep = oracle.typed_sort_rows(keys, pay, family=family, descending=desc,
+                                                    unique=(tie == "unique"))
+                    kt = torch.from_numpy(keys).cuda()
+                    pt = torch.from_numpy(pay.view(np.int32 if pdt == "uint32" else np.int64)).cuda() \
+                        if pay is not None else None
+                    if pt is not None:
+                        pt = pt.view(torch.uint32 if pdt == "uint32" else torch.uint64)
+                    gk, gp = batch.sort_rows(kt, pt, family=family, descending=desc, tie=tie)
+                    torch.cuda.synchronize()
+                    gk = gk.cpu().numpy()
+                    assert np.array_equal(gk.view(np.uint8), ek.view(np.uint8)), (n, family, tie, desc)
+                    if pay is not None:
+                        assert np.array_equal(gp.cpu().numpy().view(pay.dtype), ep), (n, family, tie, desc)
+
+
+def test_sort_rows_inplace_and_host_path(torch):
+    from paper_2002_05599_b200 import batch
+    rng = np.random.default_rng(1)
+    keys = rng.integers(0, 2**64, size=(5000, 16), dtype=np.uint64)
+    pay = rng.integers(0, 2**32, size=(5000, 16), dtype=np.uint64).astype(np.uint32)
+    ek, ep = oracle.typed_sort_rows(keys, pay)
+    hk, hp = batch.sort_rows(keys, pay)               # host buffers
+    assert np.array_equal(hk, ek) and np.array_equal(hp, ep)
+    kt = torch.from_numpy(keys.view(np.int64)).cuda().view(torch.uint64)
+    pt = torch.from_numpy(pay.view(np.int32)).cuda().view(torch.uint32)
+    batch.sort_rows(kt, pt, out_keys=kt, out_payload=pt)  # in place
+    assert np.array_equal(kt.cpu().numpy(), ek) and np.array_equal(pt.cpu().numpy(), ep)
+
+
+@pytest.mark.parametrize("rows", [1, 2, 31, 32, 33, 127, 129, 511, 513, 4095, 4097, 65537])
+def test_ragged_row_counts(rows, torch):
+    from paper_2002_05599_b200 import batch
+    rng = np.random.default_rng(rows)
+    for n in (2, 3, 5, 8, 13, 16):
+        keys = rng.integers(0, 2**32, size=(rows, n), dtype=np.uint64).astype(np.uint32)
+        k, _ = batch.sort_rows(torch.from_numpy(keys.view(np.int32)).cuda().view(torch.uint32))
+        assert np.array_equal(k.cpu().numpy(), np.sort(keys, axis=1))
+
+
+def test_misaligned_device_pointer_rejected(torch):
+    from paper_2002_05599_b200 import batch
+    from paper_2002_05599_b200.errors import ConfigurationError
+    buf = torch.zeros(1000 * 3 + 1, dtype=torch.int32, device="cuda")
+    with pytest.raises(ConfigurationError):
+        batch.sort_rows(buf[1:].view(1000, 3))
+
+
+# ---------------------------------------------------------------------------
+# BASELINE sizes: size-independent properties, checked on the device with
+# torch.sort as an independent sorter
+# ---------------------------------------------------------------------------
+
+def test_cfg1_full_size(torch):
+    """cfg1: 2^20 rows x 8 uint32, best_08: bit-exact vs torch.sort and the oracle."""
+    from paper_2002_05599_b200 import batch
+    keys = oracle.splitmix(2**20 * 8, seed=1, elem_bytes=4).reshape(2**20, 8)
+    k, _ = batch.sort_rows(torch.from_numpy(keys.view(np.int32)).cuda().view(torch.uint32))
+    got = k.cpu().numpy()
+    assert np.array_equal(got, np.sort(keys, axis=1))
+    ek, _ = oracle.typed_sort_rows(keys[:4096], None)
+    assert np.array_equal(got[:4096], ek)
+
+
+@pytest.mark.parametrize("n", [2, 7, 12, 16])
+def test_cfg2_full_size_properties(n, torch):
+    """cfg2: 2^24 rows of n uint64 (+u32 payload), best and BN: sorted rows equal torch.sort."""
+    from paper_2002_05599_b200 import batch
+    rows = 2**24
+    dev = torch.device("cuda")
+    raw = torch.randint(-2**63, 2**63 - 1, (rows, n), dtype=torch.int64, device=dev)
+    keys = raw.view(torch.uint64)
+    pay = torch.arange(n, dtype=torch.int32, device=dev).repeat(rows, 1).view(torch.uint32)
+    biased = raw ^ torch.tensor(-2**63, dtype=torch.int64, device=dev)  # u64 order as i64 order
+    ref_sorted, ref_idx = torch.sort(biased, dim=1, stable=True)
+    for family in ("best", "bn-l"):
+        k, _ = batch.sort_rows(keys, family=family)
+        assert torch.equal((k.view(torch.int64) ^ torch.tensor(-2**63, dtype=torch.int64, device=dev)),
+                           ref_sorted), family
+        k, p = batch.sort_rows(keys, pay, family=family, tie="unique")
+        assert torch.equal(k.view(torch.int64) ^ torch.tensor(-2**63, dtype=torch.int64, device=dev),
+                           ref_sorted)
+        ties = (ref_sorted[:, 1:] == ref_sorted[:, :-1]).any(dim=1)
+        ok = torch.equal(p.view(torch.int32)[~ties], ref_idx.to(torch.int32)[~ties])
+        assert ok, family
+    del raw, keys, pay, biased, ref_sorted, ref_idx
+    torch.cuda.empty_cache()
+
+
+def test_cfg5_shard_properties(torch):
+    """cfg5 on one shard (2^24 of the 2^28 arrays): n=16 u64 key + u64 global index, UNIQUE."""
+    from paper_2002_05599_b200 import batch
+    rows, n = 2**24, 16
+    dev = torch.device("cuda")
+    raw = torch.randint(-2**63, 2**63 - 1, (rows, n), dtype=torch.int64, device=dev)
+    idx = torch.arange(rows * n, dtype=torch.int64, device=dev).view(rows, n)
+    k, p = batch.sort_rows(raw.view(torch.uint64), idx.view(torch.uint64))
+    sign = torch.tensor(-2**63, dtype=torch.int64, device=dev)
+    ref_sorted, ref_idx = torch.sort(raw ^ sign, dim=1, stable=True)
+    assert torch.equal(k.view(torch.int64) ^ sign, ref_sorted)
+    ties = (ref_sorted[:, 1:] == ref_sorted[:, :-1]).any(dim=1)
+    exp_p = torch.gather(idx, 1, ref_idx)
+    assert torch.equal(p.view(torch.int64)[~ties], exp_p[~ties])
+    # payload is a permutation of the row's global indices (checksum of checksums)
+    assert torch.equal(p.view(torch.int64).sum(dim=1), idx.sum(dim=1))

@@ -79,6 +79,9 @@ def sort_rows(keys, payload=None, *, kind: str = "network", family: str = "best"
     if _is_torch(keys):
         if not keys.is_cuda or not keys.is_contiguous():
             raise ConfigurationError("keys must be a contiguous CUDA tensor")
+        for t in (keys, payload, out_keys, out_payload):
+            if t is not None and t.data_ptr() % 16:
+                raise ConfigurationError("device buffers must be 16-byte aligned")
         ok = out_keys if out_keys is not None else keys.new_empty(keys.shape)
         op = None
         if payload is not None:

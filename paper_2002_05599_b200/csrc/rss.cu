@@ -1,9 +1,519 @@
+// Register Sample Sort, one WARP per array (n <= 1024).
+//
+// Restates the reference recursion `ns_rss_rec` (netsort_core.c:325-391) and
+// its base case `ns_small_base` (:309-323) so that outputs are bit-identical
+// to the reference even with payloads under key ties (REF mode):
+//
+//  * the LCG draws are consumed in the reference's depth-first order: ranges
+//    are processed from an explicit stack (children pushed 3..0 so bucket 0
+//    is popped first), and every range that samples advances the state by
+//    `4a` draws.  The draws themselves are computed in parallel: lane t takes
+//    state * 48271^(t+1) mod (2^31-1) from a constant power table;
+//  * the 4a-key sample is ranked across lanes (its sorted key sequence is
+//    unique, so the splitters equal the reference's smp[a-1], smp[2a-1],
+//    smp[3a-1]);
+//  * classification is the reference's branch-free rule
+//    tag = ((s1<k)<<1) + ((s1<k ? s2 : s0) < k)  (NS_CLS_LANE, :270-274);
+//  * the scatter is STABLE (warp ballots + popc prefix per 32-element chunk),
+//    exactly like the reference's counting scatter (:375-382); it goes to the
+//    other shared-memory buffer instead of memcpy'ing back;
+//  * leaves are deferred (they consume no draws) and run lane-parallel at the
+//    end: exact-size networks from csrc/gen/nets.cuh for <= 16 items, stable
+//    insertion sort (ns_ins_def) for the degenerate / deep / IS-base cases.
+//
+// UNIQUE mode (typed batches with payload) classifies by key exactly the same
+// way and orders leaves lexicographically by (key, payload).
+#include "common.cuh"
+#include "gen/nets.cuh"
 #include "kernels.cuh"
+#include "net_sort.cuh"
+
 namespace nsg {
-int launch_rss_rows(const nsg_spec&, const void*, void*, const void*, void*, int64_t, int64_t, cudaStream_t) {
-  return fail(NSG_ERR_SPEC, "RSS not built yet");
+
+namespace {
+
+constexpr uint32_t kLcgM = 2147483647u;
+
+struct LcgPow {
+  uint32_t p[65];
+};
+constexpr LcgPow make_lcg_pow() {
+  LcgPow t{};
+  uint64_t v = 1;
+  for (int j = 0; j < 65; ++j) {
+    t.p[j] = uint32_t(v);
+    v = (v * 48271u) % kLcgM;
+  }
+  return t;
 }
-int launch_rss_items(const nsg_spec&, void*, int64_t, int64_t, cudaStream_t) {
-  return fail(NSG_ERR_SPEC, "RSS not built yet");
+__constant__ LcgPow c_lcg_pow = make_lcg_pow();
+
+__device__ __forceinline__ uint32_t lcg_jump(uint32_t s, int j) {  // lcg^j(s)
+  return uint32_t((uint64_t(s) * c_lcg_pow.p[j]) % kLcgM);
 }
+
+struct RssParams {
+  const void* k_in;
+  void* k_out;
+  const void* p_in;
+  void* p_out;
+  int64_t rows;
+  int n;
+  int threshold;
+  int oversampling;
+  int base_kind;  // 0 network, 1 insertion
+  uint32_t seed;
+  Xform xf;
+};
+
+// range / leaf descriptor: lo:11 | cnt:11 | depth:7 | buf:1 | leaf kind:2
+__device__ __forceinline__ uint32_t pack(int lo, int cnt, int depth, int buf, int kind) {
+  return uint32_t(lo) | (uint32_t(cnt) << 11) | (uint32_t(depth) << 22) | (uint32_t(buf) << 29) |
+         (uint32_t(kind) << 30);
+}
+__device__ __forceinline__ int r_lo(uint32_t e) { return int(e & 2047u); }
+__device__ __forceinline__ int r_cnt(uint32_t e) { return int((e >> 11) & 2047u); }
+__device__ __forceinline__ int r_depth(uint32_t e) { return int((e >> 22) & 127u); }
+__device__ __forceinline__ int r_buf(uint32_t e) { return int((e >> 29) & 1u); }
+__device__ __forceinline__ int r_kind(uint32_t e) { return int(e >> 30); }
+
+enum LeafKind { LEAF_NET = 0, LEAF_INS = 1 };
+
+template <class U, class P, int NMAX, int DAG, int MODE, int LAYOUT>
+struct RssCfg {
+  using Uk = U;
+  using Pk = P;
+  static constexpr bool HAS_P = !IsNoPay<P>::value;
+  static constexpr int PB = PayBytes<P>::value;
+  static constexpr int NMAX_ = NMAX;
+  static constexpr int WARPS = NMAX <= 256 ? 4 : 2;
+  // per-warp shared memory
+  static constexpr int BUF_BYTES = NMAX * (int(sizeof(U)) + PB);
+  static constexpr int OFF_A = 0;
+  static constexpr int OFF_B = BUF_BYTES;
+  static constexpr int OFF_STACK = 2 * BUF_BYTES;              // NMAX/2 u32
+  static constexpr int OFF_LEAF = OFF_STACK + NMAX / 2 * 4;    // NMAX u32
+  static constexpr int OFF_SMP = OFF_LEAF + NMAX * 4;          // 64 keys
+  static constexpr int WARP_SMEM = (OFF_SMP + 64 * 8 + 15) / 16 * 16;
+  static constexpr int CTA_SMEM = WARPS * WARP_SMEM;
+  using CX = typename std::conditional<!HAS_P, CxKeys,
+                                       typename std::conditional<MODE == MODE_REF, CxRef, CxUnique>::type>::type;
+};
+
+template <class Cfg>
+struct WarpBufs {
+  using U = typename Cfg::Uk;
+  using P = typename Cfg::Pk;
+  unsigned char* base;
+  __device__ U* keys(int b) const { return reinterpret_cast<U*>(base + (b ? Cfg::OFF_B : Cfg::OFF_A)); }
+  __device__ P* pays(int b) const {
+    return reinterpret_cast<P*>(base + (b ? Cfg::OFF_B : Cfg::OFF_A) + sizeof(U) * Cfg::NMAX_);
+  }
+  __device__ uint32_t* stack() const { return reinterpret_cast<uint32_t*>(base + Cfg::OFF_STACK); }
+  __device__ uint32_t* leaves() const { return reinterpret_cast<uint32_t*>(base + Cfg::OFF_LEAF); }
+  __device__ U* smp() const { return reinterpret_cast<U*>(base + Cfg::OFF_SMP); }
+};
+
+// element order used by leaves: REF = key only (stable where it matters),
+// UNIQUE = (key, payload)
+template <class Cfg>
+__device__ __forceinline__ bool elem_less(typename Cfg::Uk bk, const typename Cfg::Pk& bp, typename Cfg::Uk ak,
+                                          const typename Cfg::Pk& ap) {
+  if constexpr (Cfg::HAS_P && std::is_same<typename Cfg::CX, CxUnique>::value) {
+    return bk < ak || (bk == ak && bp < ap);
+  } else {
+    return bk < ak;
+  }
+}
+
+// Exact-size network on <= 16 items held in registers (REF-mode DAG parity).
+template <class Cfg, int DAG>
+__device__ __forceinline__ void leaf_network(Elem<typename Cfg::Uk, typename Cfg::Pk>* v, int cnt) {
+  using CX = typename Cfg::CX;
+  switch (cnt) {
+    case 2: Net<DAG, 2>::template run<CX>(v); break;
+    case 3: Net<DAG, 3>::template run<CX>(v); break;
+    case 4: Net<DAG, 4>::template run<CX>(v); break;
+    case 5: Net<DAG, 5>::template run<CX>(v); break;
+    case 6: Net<DAG, 6>::template run<CX>(v); break;
+    case 7: Net<DAG, 7>::template run<CX>(v); break;
+    case 8: Net<DAG, 8>::template run<CX>(v); break;
+    case 9: Net<DAG, 9>::template run<CX>(v); break;
+    case 10: Net<DAG, 10>::template run<CX>(v); break;
+    case 11: Net<DAG, 11>::template run<CX>(v); break;
+    case 12: Net<DAG, 12>::template run<CX>(v); break;
+    case 13: Net<DAG, 13>::template run<CX>(v); break;
+    case 14: Net<DAG, 14>::template run<CX>(v); break;
+    case 15: Net<DAG, 15>::template run<CX>(v); break;
+    case 16: Net<DAG, 16>::template run<CX>(v); break;
+    default: break;
+  }
+}
+
+template <class U, class P, int NMAX, int DAG, int MODE, int LAYOUT>
+__global__ void __launch_bounds__(RssCfg<U, P, NMAX, DAG, MODE, LAYOUT>::WARPS * 32)
+    rss_kernel(const RssParams prm) {
+  using Cfg = RssCfg<U, P, NMAX, DAG, MODE, LAYOUT>;
+  using E = Elem<U, P>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  WarpBufs<Cfg> wb{smem_raw + warp * Cfg::WARP_SMEM};
+  const int n = prm.n;
+  const int a = prm.oversampling;
+  const int sample = 4 * a;
+  const Xform xf = prm.xf;
+
+  for (int64_t row = int64_t(blockIdx.x) * Cfg::WARPS + warp; row < prm.rows;
+       row += int64_t(gridDim.x) * Cfg::WARPS) {
+    // ---- load the row into buffer A (ordered-key space) --------------------
+    U* ka = wb.keys(0);
+    P* pa = wb.pays(0);
+    if constexpr (LAYOUT == LAYOUT_AOS16) {
+      const uint4* src = static_cast<const uint4*>(prm.k_in) + row * n;
+      for (int i = lane; i < n; i += 32) {
+        const uint4 it = src[i];
+        ka[i] = U(uint64_t(it.x) | (uint64_t(it.y) << 32));
+        if constexpr (Cfg::HAS_P) pa[i] = P(uint64_t(it.z) | (uint64_t(it.w) << 32));
+      }
+    } else {
+      const U* ks = static_cast<const U*>(prm.k_in) + row * n;
+      for (int i = lane; i < n; i += 32) {
+        U k = ks[i];
+        if (xf.active) k = to_ord<U>(k, xf);
+        ka[i] = k;
+        if constexpr (Cfg::HAS_P) {
+          P p = static_cast<const P*>(prm.p_in)[row * n + i];
+          if (xf.active) p ^= P(xf.pdesc);
+          pa[i] = p;
+        }
+      }
+    }
+    uint32_t* stk = wb.stack();
+    uint32_t* leaf = wb.leaves();
+    int sp = 0;          // stack depth (warp-uniform)
+    int nleaf_net = 0;   // leaves from the front
+    int nleaf_ins = 0;   // leaves from the back
+    uint32_t state = prm.seed;
+    if (lane == 0) stk[0] = pack(0, n, 0, 0, 0);
+    sp = 1;
+    __syncwarp();
+
+    auto add_leaf = [&](int lo, int cnt, int buf, int kind) {
+      if (kind == LEAF_NET) {
+        if (lane == 0) leaf[nleaf_net] = pack(lo, cnt, 0, buf, LEAF_NET);
+        ++nleaf_net;
+      } else {
+        ++nleaf_ins;
+        if (lane == 0) leaf[NMAX - nleaf_ins] = pack(lo, cnt, 0, buf, LEAF_INS);
+      }
+    };
+    // ns_small_base (netsort_core.c:309-323)
+    auto small_base = [&](int lo, int cnt, int buf) {
+      if (cnt < 2) {
+        if (cnt == 1) add_leaf(lo, 1, buf, LEAF_NET);
+        return;
+      }
+      if (prm.base_kind == 0 && cnt <= 16)
+        add_leaf(lo, cnt, buf, LEAF_NET);
+      else
+        add_leaf(lo, cnt, buf, LEAF_INS);
+    };
+
+    while (sp > 0) {
+      const uint32_t e = stk[sp - 1];
+      __syncwarp();
+      --sp;
+      const int lo = r_lo(e), cnt = r_cnt(e), depth = r_depth(e), buf = r_buf(e);
+      if (cnt <= prm.threshold) {
+        small_base(lo, cnt, buf);
+        continue;
+      }
+      if (cnt < sample) {
+        if (cnt <= 16)
+          small_base(lo, cnt, buf);
+        else
+          add_leaf(lo, cnt, buf, LEAF_INS);
+        continue;
+      }
+      if (depth >= 64 || sample > 64) {
+        add_leaf(lo, cnt, buf, LEAF_INS);
+        continue;
+      }
+      const U* kb = wb.keys(buf) + lo;
+      // ---- sample: draws state^(t+1), t = 0..sample-1 ---------------------
+      U* smp = wb.smp();
+      U s_a = U(0), s_b = U(0);
+      const bool has_a = lane < sample, has_b = lane + 32 < sample;
+      if (has_a) s_a = kb[lcg_jump(state, lane + 1) % uint32_t(cnt)];
+      if (has_b) s_b = kb[lcg_jump(state, lane + 33) % uint32_t(cnt)];
+      state = lcg_jump(state, sample);
+      // rank among the sample (ties broken by draw index -> a total order)
+      int ra = 0, rb = 0;
+      for (int u = 0; u < sample; ++u) {
+        const U ku = u < 32 ? __shfl_sync(0xffffffffu, s_a, u) : __shfl_sync(0xffffffffu, s_b, u - 32);
+        ra += (ku < s_a) || (ku == s_a && u < lane);
+        rb += (ku < s_b) || (ku == s_b && u < lane + 32);
+      }
+      if (has_a) smp[ra] = s_a;
+      if (has_b) smp[rb] = s_b;
+      __syncwarp();
+      const U s0 = smp[a - 1], s1 = smp[2 * a - 1], s2 = smp[3 * a - 1];
+      __syncwarp();
+      // ---- count -----------------------------------------------------------
+      int c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+      for (int i = lane; i < cnt; i += 32) {
+        const U k = kb[i];
+        const bool c = s1 < k;
+        const U x = c ? s2 : s0;
+        const int tag = (int(c) << 1) + int(x < k);
+        c0 += tag == 0; c1 += tag == 1; c2 += tag == 2; c3 += tag == 3;
+      }
+      c0 = __reduce_add_sync(0xffffffffu, c0);
+      c1 = __reduce_add_sync(0xffffffffu, c1);
+      c2 = __reduce_add_sync(0xffffffffu, c2);
+      c3 = __reduce_add_sync(0xffffffffu, c3);
+      const int big = max(max(c0, c1), max(c2, c3));
+      if (big == cnt) {  // no progress possible: insertion sort (netsort_core.c:370-373)
+        add_leaf(lo, cnt, buf, LEAF_INS);
+        continue;
+      }
+      // ---- stable scatter into the other buffer ---------------------------
+      const int ob = buf ^ 1;
+      U* ko = wb.keys(ob) + lo;
+      P* po = wb.pays(ob) + lo;
+      const P* pb = wb.pays(buf) + lo;
+      int o0 = 0, o1 = c0, o2 = c0 + c1, o3 = c0 + c1 + c2;
+      for (int base = 0; base < cnt; base += 32) {
+        const int i = base + lane;
+        const bool live = i < cnt;
+        U k = U(0);
+        int tag = -1;
+        if (live) {
+          k = kb[i];
+          const bool c = s1 < k;
+          const U x = c ? s2 : s0;
+          tag = (int(c) << 1) + int(x < k);
+        }
+        const unsigned m0 = __ballot_sync(0xffffffffu, tag == 0);
+        const unsigned m1 = __ballot_sync(0xffffffffu, tag == 1);
+        const unsigned m2 = __ballot_sync(0xffffffffu, tag == 2);
+        const unsigned m3 = __ballot_sync(0xffffffffu, tag == 3);
+        if (live) {
+          const unsigned mm = tag == 0 ? m0 : tag == 1 ? m1 : tag == 2 ? m2 : m3;
+          const int ob_ = tag == 0 ? o0 : tag == 1 ? o1 : tag == 2 ? o2 : o3;
+          const int pos = ob_ + __popc(mm & lt_mask);
+          ko[pos] = k;
+          if constexpr (Cfg::HAS_P) po[pos] = pb[i];
+        }
+        o0 += __popc(m0); o1 += __popc(m1); o2 += __popc(m2); o3 += __popc(m3);
+      }
+      __syncwarp();
+      // ---- children, bucket 0 on top of the stack -------------------------
+      const int cs[4] = {c0, c1, c2, c3};
+      const int st[4] = {0, c0, c0 + c1, c0 + c1 + c2};
+#pragma unroll
+      for (int b = 3; b >= 0; --b) {
+        if (cs[b] > 1) {
+          if (lane == 0) stk[sp] = pack(lo + st[b], cs[b], depth + 1, ob, 0);
+          ++sp;
+        } else if (cs[b] == 1) {
+          add_leaf(lo + st[b], 1, ob, LEAF_NET);
+        }
+      }
+      __syncwarp();
+    }
+    __syncwarp();
+
+    // ---- leaves: lane-parallel; results land in buffer A -------------------
+    for (int li = lane; li < nleaf_net; li += 32) {
+      const uint32_t e = leaf[li];
+      const int lo = r_lo(e), cnt = r_cnt(e), buf = r_buf(e);
+      const U* ks = wb.keys(buf) + lo;
+      const P* ps = wb.pays(buf) + lo;
+      E v[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (j < cnt) {
+          v[j].k = ks[j];
+          if constexpr (Cfg::HAS_P) v[j].p = ps[j];
+        }
+      }
+      leaf_network<Cfg, DAG>(v, cnt);
+      U* kd = wb.keys(0) + lo;
+      P* pd = wb.pays(0) + lo;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (j < cnt) {
+          kd[j] = v[j].k;
+          if constexpr (Cfg::HAS_P) pd[j] = v[j].p;
+        }
+      }
+    }
+    // stable insertion sort (ns_ins_def, netsort_core.c:124-134), in place in
+    // its buffer, then moved to A
+    for (int li = lane; li < nleaf_ins; li += 32) {
+      const uint32_t e = leaf[NMAX - 1 - li];
+      const int lo = r_lo(e), cnt = r_cnt(e), buf = r_buf(e);
+      U* ks = wb.keys(buf) + lo;
+      P* ps = wb.pays(buf) + lo;
+      for (int i = 1; i < cnt; ++i) {
+        const U vk = ks[i];
+        P vp{};
+        if constexpr (Cfg::HAS_P) vp = ps[i];
+        int j = i - 1;
+        while (j >= 0) {
+          bool lt;
+          if constexpr (Cfg::HAS_P)
+            lt = elem_less<Cfg>(vk, vp, ks[j], ps[j]);
+          else
+            lt = vk < ks[j];
+          if (!lt) break;
+          ks[j + 1] = ks[j];
+          if constexpr (Cfg::HAS_P) ps[j + 1] = ps[j];
+          --j;
+        }
+        ks[j + 1] = vk;
+        if constexpr (Cfg::HAS_P) ps[j + 1] = vp;
+      }
+      if (buf != 0) {
+        U* kd = wb.keys(0) + lo;
+        P* pd = wb.pays(0) + lo;
+        for (int i = 0; i < cnt; ++i) {
+          kd[i] = ks[i];
+          if constexpr (Cfg::HAS_P) pd[i] = ps[i];
+        }
+      }
+    }
+    __syncwarp();
+
+    // ---- write the row out (coalesced) -------------------------------------
+    if constexpr (LAYOUT == LAYOUT_AOS16) {
+      uint4* dst = static_cast<uint4*>(prm.k_out) + row * n;
+      for (int i = lane; i < n; i += 32) {
+        const uint64_t k = uint64_t(ka[i]);
+        uint64_t p = 0;
+        if constexpr (Cfg::HAS_P) p = uint64_t(pa[i]);
+        dst[i] = make_uint4(uint32_t(k), uint32_t(k >> 32), uint32_t(p), uint32_t(p >> 32));
+      }
+    } else {
+      U* kd = static_cast<U*>(prm.k_out) + row * n;
+      for (int i = lane; i < n; i += 32) {
+        U k = ka[i];
+        if (xf.active) k = from_ord<U>(k, xf);
+        kd[i] = k;
+        if constexpr (Cfg::HAS_P) {
+          P p = pa[i];
+          if (xf.active) p ^= P(xf.pdesc);
+          static_cast<P*>(prm.p_out)[row * n + i] = p;
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+struct RssKernel {
+  const void* fn;
+  int smem;
+  int threads;
+  int warps;
+};
+
+template <class U, class P, int NMAX, int DAG, int MODE, int LAYOUT>
+RssKernel rss_info_n() {
+  using Cfg = RssCfg<U, P, NMAX, DAG, MODE, LAYOUT>;
+  return {reinterpret_cast<const void*>(&rss_kernel<U, P, NMAX, DAG, MODE, LAYOUT>), Cfg::CTA_SMEM,
+          Cfg::WARPS * 32, Cfg::WARPS};
+}
+
+template <int NMAX, int DAG>
+RssKernel rss_pick_dag(int key_bytes, int pay, int mode, int layout) {
+  if (layout == LAYOUT_AOS16)
+    return mode ? rss_info_n<uint64_t, uint64_t, NMAX, DAG, MODE_UNIQUE, LAYOUT_AOS16>()
+                : rss_info_n<uint64_t, uint64_t, NMAX, DAG, MODE_REF, LAYOUT_AOS16>();
+  if (key_bytes == 4) {
+    if (pay == 0) return rss_info_n<uint32_t, NoPay, NMAX, DAG, MODE_UNIQUE, LAYOUT_SOA>();
+    if (pay == 1)
+      return mode ? rss_info_n<uint32_t, uint32_t, NMAX, DAG, MODE_UNIQUE, LAYOUT_SOA>()
+                  : rss_info_n<uint32_t, uint32_t, NMAX, DAG, MODE_REF, LAYOUT_SOA>();
+    return mode ? rss_info_n<uint32_t, uint64_t, NMAX, DAG, MODE_UNIQUE, LAYOUT_SOA>()
+                : rss_info_n<uint32_t, uint64_t, NMAX, DAG, MODE_REF, LAYOUT_SOA>();
+  }
+  if (pay == 0) return rss_info_n<uint64_t, NoPay, NMAX, DAG, MODE_UNIQUE, LAYOUT_SOA>();
+  if (pay == 1)
+    return mode ? rss_info_n<uint64_t, uint32_t, NMAX, DAG, MODE_UNIQUE, LAYOUT_SOA>()
+                : rss_info_n<uint64_t, uint32_t, NMAX, DAG, MODE_REF, LAYOUT_SOA>();
+  return mode ? rss_info_n<uint64_t, uint64_t, NMAX, DAG, MODE_UNIQUE, LAYOUT_SOA>()
+              : rss_info_n<uint64_t, uint64_t, NMAX, DAG, MODE_REF, LAYOUT_SOA>();
+}
+
+RssKernel rss_pick(int n, int dag, int key_bytes, int pay, int mode, int layout) {
+  if (n <= 256)
+    return dag ? rss_pick_dag<256, 1>(key_bytes, pay, mode, layout) : rss_pick_dag<256, 0>(key_bytes, pay, mode, layout);
+  return dag ? rss_pick_dag<1024, 1>(key_bytes, pay, mode, layout) : rss_pick_dag<1024, 0>(key_bytes, pay, mode, layout);
+}
+
+int launch_rss(const nsg_spec& sp, const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows,
+               int64_t n, int key_bytes, int pay, int mode, int layout, const Xform& xf, cudaStream_t st) {
+  if (n > 1024) return fail(NSG_ERR_SPEC, "RSS rows are limited to 1024 items on the device, got %lld", (long long)n);
+  if (sp.kind == NSG_KIND_RSS) {
+    if (sp.rss_oversampling < 1 || sp.rss_oversampling > 16)
+      return fail(NSG_ERR_SPEC, "RSS oversampling %d not in 1..16", sp.rss_oversampling);
+    if (sp.rss_threshold < 2) return fail(NSG_ERR_SPEC, "RSS threshold must be >= 2");
+    if (sp.base_kind == 0 && sp.rss_threshold > 16)
+      return fail(NSG_ERR_SPEC, "network base case caps the threshold at 16");
+  }
+  RssParams prm{};
+  prm.k_in = k_in;
+  prm.k_out = k_out;
+  prm.p_in = p_in;
+  prm.p_out = p_out;
+  prm.rows = rows;
+  prm.n = int(n);
+  if (sp.kind == NSG_KIND_INSERTION) {  // stable insertion sort of the whole row
+    prm.threshold = 1 << 20;
+    prm.oversampling = 1;
+    prm.base_kind = 1;
+  } else {
+    prm.threshold = sp.rss_threshold;
+    prm.oversampling = sp.rss_oversampling;
+    prm.base_kind = sp.base_kind;
+  }
+  prm.seed = sp.rss_sample_seed;
+  prm.xf = xf;
+  const RssKernel k = rss_pick(int(n), sp.family == 0 ? 0 : 1, key_bytes, pay, mode, layout);
+  int dev = 0, sms = 0, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (k.smem > 48 * 1024) cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, k.smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k.fn, k.threads, k.smem);
+  if (occ < 1) return fail(NSG_ERR_CUDA, "RSS kernel cannot be resident (smem %d)", k.smem);
+  const int64_t need = (rows + k.warps - 1) / k.warps;
+  const int64_t grid = need < int64_t(sms) * occ ? need : int64_t(sms) * occ;
+  void* args[] = {&prm};
+  const cudaError_t e = cudaLaunchKernel(k.fn, dim3(unsigned(grid)), dim3(unsigned(k.threads)), args, size_t(k.smem), st);
+  if (e != cudaSuccess) return fail(NSG_ERR_CUDA, "rss_kernel launch: %s", cudaGetErrorString(e));
+  return 0;
+}
+
+}  // namespace
+
+static int key_bytes_of(int dt) {
+  return (dt == NSG_KEY_U32 || dt == NSG_KEY_I32 || dt == NSG_KEY_F32) ? 4 : 8;
+}
+
+int launch_rss_rows(const nsg_spec& sp, const void* keys_in, void* keys_out, const void* pay_in, void* pay_out,
+                    int64_t rows, int64_t n, cudaStream_t st) {
+  if (rows <= 0 || n <= 0) return 0;
+  return launch_rss(sp, keys_in, keys_out, pay_in, pay_out, rows, n, key_bytes_of(sp.key_dtype), sp.payload_dtype,
+                    sp.tie_mode, LAYOUT_SOA, make_xform(sp), st);
+}
+
+int launch_rss_items(const nsg_spec& sp, void* rows, int64_t m, int64_t n, cudaStream_t st) {
+  if (m <= 0 || n <= 0) return 0;
+  return launch_rss(sp, rows, rows, nullptr, nullptr, m, n, 8, 2, MODE_REF, LAYOUT_AOS16, Xform{}, st);
+}
+
 }  // namespace nsg

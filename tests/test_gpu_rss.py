@@ -1,0 +1,158 @@
+"""GPU parity of Register Sample Sort (warp-per-array kernel) vs the oracle.
+
+REF mode is bit-exact with the reference including payload order under key
+ties, because the kernel replays the reference's LCG draws in depth-first
+order (reference test_backends.py:145-177, test_acceptance.py A06/A07,
+test_rss.py).
+"""
+
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+G = Path(__file__).parent / "golden"
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+    assert t.cuda.is_available()
+    return t
+
+
+def _items(keys, refs):
+    a = np.empty(keys.shape, dtype=oracle.ITEM)
+    a["key"], a["ref"] = keys, refs
+    return a
+
+
+def test_rss_matches_reference_golden(torch):
+    from paper_2002_05599_b200 import backend, registry
+    rss_rows = np.load(G / "rss_rows.npz")
+    for meta in json.loads((G / "rss_meta.json").read_text()):
+        t = meta["tag"]
+        keys = rss_rows[f"in_key_{t}"]
+        rows = _items(keys, np.arange(keys.size, dtype=np.uint64).reshape(keys.shape))
+        spec = registry.spec_rss(meta["cfg"], meta["base"])
+        assert list(spec) == meta["spec"]
+        backend.run_sorter_many(spec, rows)
+        assert np.array_equal(rows["key"], rss_rows[f"out_key_{t}"]), t
+        assert np.array_equal(rows["ref"], rss_rows[f"out_ref_{t}"]), t
+
+
+@pytest.mark.parametrize("cfg,base", [("332", "SN Best 4CmS"), ("333", "SN BN-L 4CmS"), ("341", "IS Def"),
+                                      ("315", "SN BN-R TCOp"), ("391", "SN Best 4CmS"), ("311", "SN Best 4CmS")])
+def test_rss_random_vs_oracle(cfg, base, torch):
+    from paper_2002_05599_b200 import backend, registry
+    rng = np.random.default_rng(int(cfg))
+    spec = registry.spec_rss(cfg, base)
+    fam = "best"
+    kind_base = "ins" if base.startswith("IS") else "net"
+    if base.startswith("SN"):
+        fam = {"Best": "best", "BN-L": "bn-l", "BN-P": "bn-p", "BN-R": "bn-r"}[base.split()[1]]
+    for n in (2, 16, 17, 20, 35, 64, 100, 255, 256, 257, 700, 1024):
+        for gen in ("u64", "dup", "few", "sorted", "rev", "equal"):
+            m = 64
+            if gen == "u64":
+                keys = rng.integers(0, 2**64, size=(m, n), dtype=np.uint64)
+            elif gen == "dup":
+                keys = rng.integers(0, 4, size=(m, n), dtype=np.uint64)
+            elif gen == "few":
+                keys = rng.integers(0, 2**64, size=16, dtype=np.uint64)[rng.integers(0, 16, size=(m, n))]
+            elif gen == "sorted":
+                keys = np.sort(rng.integers(0, 2**64, size=(m, n), dtype=np.uint64), axis=1)
+            elif gen == "rev":
+                keys = np.sort(rng.integers(0, 2**64, size=(m, n), dtype=np.uint64), axis=1)[:, ::-1].copy()
+            else:
+                keys = np.full((m, n), 77, dtype=np.uint64)
+            refs = np.arange(m * n, dtype=np.uint64).reshape(m, n)
+            exp = _items(keys, refs)
+            oracle.run_items(exp, kind="rss", family=fam, rss_cfg=cfg, base=kind_base)
+            got = _items(keys, refs)
+            backend.run_sorter_many(spec, got)
+            assert np.array_equal(got, exp), (cfg, base, n, gen)
+
+
+def test_rss_sort_api(torch):
+    from paper_2002_05599_b200 import rss
+    from paper_2002_05599_b200.items import items_from_keys, items_from_pairs
+    arr = items_from_pairs([(42, i) for i in range(256)])
+    rss.rss_sort(arr, rss.RssConfig.from_string("332"))
+    assert arr["key"].tolist() == [42] * 256 and sorted(arr["ref"].tolist()) == list(range(256))
+    arr = items_from_keys(list(range(300)))
+    rss.rss_sort(arr, rss.RssConfig.from_string("341"))
+    assert arr["key"].tolist() == list(range(300))
+    rng = np.random.default_rng(12)
+    cfg = rss.RssConfig.from_string("391")
+    for n in range(17, 36):  # 16 < n < 4a: too small to sample
+        keys = rng.integers(0, 2**64, size=n, dtype=np.uint64)
+        arr = items_from_keys(keys)
+        rss.rss_sort(arr, cfg)
+        assert np.array_equal(arr["key"], np.sort(keys))
+
+
+def test_insertion_kind_is_stable(torch):
+    from paper_2002_05599_b200 import backend, registry
+    rng = np.random.default_rng(3)
+    for n in (2, 9, 16, 40, 300):
+        keys = rng.integers(0, 3, size=(50, n), dtype=np.uint64)
+        refs = np.arange(50 * n, dtype=np.uint64).reshape(50, n)
+        got = _items(keys, refs)
+        backend.run_sorter_many(registry.spec_insertion("Def"), got)
+        order = np.argsort(keys, axis=1, kind="stable")
+        assert np.array_equal(got["key"], np.take_along_axis(keys, order, 1))
+        assert np.array_equal(got["ref"], np.take_along_axis(refs, order, 1))
+
+
+@pytest.mark.parametrize("kdt", ["int64", "uint64", "uint32", "float32"])
+@pytest.mark.parametrize("pdt", [None, "uint32", "uint64"])
+def test_rss_typed_rows_vs_oracle(kdt, pdt, torch):
+    from paper_2002_05599_b200 import batch
+    rng = np.random.default_rng(7)
+    for n in (32, 64, 128, 256):
+        for tie in (["unique"] if pdt is None else ["unique", "ref"]):
+            for desc in (False, True):
+                if kdt.startswith("float"):
+                    keys = np.round(rng.standard_normal((300, n)) * 4).astype(kdt)
+                else:
+                    info = np.iinfo(kdt)
+                    keys = rng.integers(info.min, info.max, size=(300, n), dtype=kdt, endpoint=True)
+                    keys[::3] = keys[::3] % 5
+                pay = None if pdt is None else rng.integers(0, 2**31, size=(300, n)).astype(pdt)
+                ek, ep = oracle.typed_sort_rows(keys, pay, descending=desc, unique=tie == "unique", kind="rss")
+                kt = torch.from_numpy(keys).cuda()
+                pt = None
+                if pay is not None:
+                    pt = torch.from_numpy(pay.view(np.int32 if pdt == "uint32" else np.int64)).cuda()
+                    pt = pt.view(torch.uint32 if pdt == "uint32" else torch.uint64)
+                gk, gp = batch.sort_rows(kt, pt, kind="rss", descending=desc, tie=tie)
+                assert np.array_equal(gk.cpu().numpy().view(np.uint8), ek.view(np.uint8)), (n, tie, desc)
+                if pay is not None:
+                    assert np.array_equal(gp.cpu().numpy().view(pay.dtype), ep), (n, tie, desc)
+
+
+@pytest.mark.parametrize("n", [32, 64, 128, 256])
+def test_cfg3_full_size_distributions(n, torch):
+    """cfg3: 2^20 arrays of n int64 keys, four distributions; equal to torch.sort."""
+    from paper_2002_05599_b200 import batch
+    rows = 2**20
+    dev = torch.device("cuda")
+    gen = torch.Generator(device=dev).manual_seed(n)
+    uni = torch.randint(-2**63, 2**63 - 1, (rows, n), dtype=torch.int64, device=dev, generator=gen)
+    vals = torch.randint(-2**63, 2**63 - 1, (16,), dtype=torch.int64, device=dev, generator=gen)
+    few = vals[torch.randint(0, 16, (rows, n), device=dev, generator=gen)]
+    srt = torch.sort(uni, dim=1).values
+    rev = torch.flip(srt, dims=[1]).contiguous()
+    for name, x in (("uniform", uni), ("few16", few), ("sorted", srt), ("reverse", rev)):
+        k, _ = batch.sort_rows(x, kind="rss")
+        assert torch.equal(k, torch.sort(x, dim=1).values), name
+    # a sampled subset against the oracle (full RSS replay)
+    sub = uni[:512].cpu().numpy()
+    ek, _ = oracle.typed_sort_rows(sub, None, kind="rss")
+    k, _ = batch.sort_rows(uni[:512].contiguous(), kind="rss")
+    assert np.array_equal(k.cpu().numpy(), ek)

@@ -233,6 +233,41 @@ def typed_sort_rows(keys: np.ndarray, payload=None, *, family: str = "best", des
     return out_keys, out_pay
 
 
+def typed_sort_segments(offsets, keys, payload=None, *, family: str = "best", descending: bool = False,
+                        unique: bool = True):
+    """Expected output of batch.sort_segments (CSR) through the oracle."""
+    keys = np.asarray(keys)
+    items = np.empty(len(keys), dtype=ITEM)
+    items["key"] = to_ord(keys, descending)
+    if payload is None:
+        items["ref"] = np.arange(len(keys), dtype=np.uint64)
+        sort_segments_items(offsets, items, family=family, unique=False)
+        return keys[items["ref"].astype(np.int64)], None
+    p = np.asarray(payload)
+    pbits = 8 * p.dtype.itemsize
+    pu = p.view(np.uint32 if pbits == 32 else np.uint64).astype(np.uint64)
+    if unique and descending:
+        pu = (~pu) & np.uint64((1 << pbits) - 1)
+    items["ref"] = pu
+    sort_segments_items(offsets, items, family=family, unique=unique)
+    out_k = from_ord(items["key"], keys.dtype, descending)
+    pu = items["ref"]
+    if unique and descending:
+        pu = (~pu) & np.uint64((1 << pbits) - 1)
+    return out_k, pu.astype(np.uint32 if pbits == 32 else np.uint64).view(p.dtype)
+
+
+def geometric_lengths(nseg: int, seed: int, p: float = 0.18, lo: int = 1, hi: int = 16) -> np.ndarray:
+    """cfg4 segment lengths: truncated geometric on lo..hi by inverse CDF of a
+    counter-based uniform (splitmix64 >> 11 / 2^53)."""
+    u = (splitmix(nseg, seed) >> np.uint64(11)).astype(np.float64) * (1.0 / 2**53)
+    q = 1.0 - p
+    span = hi - lo + 1
+    # P(L <= lo + k) = (1 - q^(k+1)) / (1 - q^span)
+    k = np.floor(np.log1p(-u * (1.0 - q**span)) / np.log(q)).astype(np.int64)
+    return (lo + np.clip(k, 0, span - 1)).astype(np.uint32)
+
+
 def from_ord(o: np.ndarray, dtype, descending: bool = False) -> np.ndarray:
     dtype = np.dtype(dtype)
     bits = dtype.itemsize * 8

@@ -223,15 +223,30 @@ int or_run_many(const or_spec* sp, const or_nets* nets, or_item* rows, int64_t m
   return st;
 }
 
-/* Segmented sort: segment s = [off[s], off[s+1]) sorted with the exact-length
- * network (<= 16) or insertion sort; rows of items. */
+/* Segmented sort (the device's cfg4 front end, no reference counterpart):
+ * segment s = [off[s], off[s+1]) sorted with the exact-length network of the
+ * family (<= 16 items) or RSS 332 with that network as base case (longer). */
 int or_sort_segments(const or_nets* nets, const uint32_t* off, int64_t nseg, or_item* items, int unique) {
+  const or_spec rs = {2, 0, 3, 16, 0x5EED, unique};
+  or_item* scratch = NULL;
+  uint8_t* tags = NULL;
+  long cap = 0;
   for (int64_t s = 0; s < nseg; s++) {
     const long len = (long)(off[s + 1] - off[s]);
-    if (len <= 16)
+    if (len <= 16) {
       or_net_apply(items + off[s], (int)len, nets, unique);
-    else
-      or_ins_def(items + off[s], len, unique);
+    } else {
+      if (len > cap) {
+        free(scratch);
+        free(tags);
+        cap = len;
+        scratch = (or_item*)malloc(sizeof(or_item) * (size_t)cap);
+        tags = (uint8_t*)malloc((size_t)cap);
+      }
+      or_run(&rs, nets, items + off[s], len, scratch, tags);
+    }
   }
+  free(scratch);
+  free(tags);
   return 0;
 }

@@ -23,6 +23,10 @@ int launch_fill_splitmix(void* out, int64_t count, int elem_bytes, uint64_t seed
 int launch_rss_rows(const nsg_spec& sp, const void* keys_in, void* keys_out, const void* pay_in, void* pay_out,
                     int64_t rows, int64_t n, cudaStream_t st);
 int launch_rss_items(const nsg_spec& sp, void* rows, int64_t m, int64_t n, cudaStream_t st);
+// long CSR segments: rows = *count entries of ids (device), each <= 1024 items
+int launch_rss_segment_list(const nsg_spec& sp, const uint32_t* offsets, const uint32_t* ids, const uint32_t* count,
+                            uint32_t* overflow, int64_t max_rows, const void* keys_in, void* keys_out,
+                            const void* pay_in, void* pay_out, cudaStream_t st);
 
 // segments.cu
 size_t segments_ws_bytes(int64_t nseg, int64_t nelem);

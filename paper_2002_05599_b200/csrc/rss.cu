@@ -64,6 +64,12 @@ struct RssParams {
   int base_kind;  // 0 network, 1 insertion
   uint32_t seed;
   Xform xf;
+  // segment-list mode (long CSR segments, csrc/segments.cu): row r is segment
+  // seg_ids[r] = [seg_off[s], seg_off[s+1]); *seg_count rows; n is then NMAX.
+  const uint32_t* seg_ids;
+  const uint32_t* seg_off;
+  const uint32_t* seg_count;
+  uint32_t* seg_overflow;
 };
 
 // range / leaf descriptor: lo:11 | cnt:11 | depth:7 | buf:1 | leaf kind:2
@@ -160,31 +166,42 @@ __global__ void __launch_bounds__(RssCfg<U, P, NMAX, DAG, MODE, LAYOUT>::WARPS *
   const int warp = threadIdx.x >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
   WarpBufs<Cfg> wb{smem_raw + warp * Cfg::WARP_SMEM};
-  const int n = prm.n;
   const int a = prm.oversampling;
   const int sample = 4 * a;
   const Xform xf = prm.xf;
 
-  for (int64_t row = int64_t(blockIdx.x) * Cfg::WARPS + warp; row < prm.rows;
+  const int64_t nrows = prm.seg_count ? min(int64_t(*prm.seg_count), prm.rows) : prm.rows;
+  for (int64_t row = int64_t(blockIdx.x) * Cfg::WARPS + warp; row < nrows;
        row += int64_t(gridDim.x) * Cfg::WARPS) {
+    int n = prm.n;
+    int64_t base = row * int64_t(prm.n);
+    if (prm.seg_ids) {
+      const uint32_t s = prm.seg_ids[row];
+      base = prm.seg_off[s];
+      n = int(prm.seg_off[s + 1] - prm.seg_off[s]);
+      if (n > NMAX) {  // longer than the per-warp buffers: counted, left unsorted
+        if (lane == 0) atomicAdd(prm.seg_overflow, 1u);
+        continue;
+      }
+    }
     // ---- load the row into buffer A (ordered-key space) --------------------
     U* ka = wb.keys(0);
     P* pa = wb.pays(0);
     if constexpr (LAYOUT == LAYOUT_AOS16) {
-      const uint4* src = static_cast<const uint4*>(prm.k_in) + row * n;
+      const uint4* src = static_cast<const uint4*>(prm.k_in) + base;
       for (int i = lane; i < n; i += 32) {
         const uint4 it = src[i];
         ka[i] = U(uint64_t(it.x) | (uint64_t(it.y) << 32));
         if constexpr (Cfg::HAS_P) pa[i] = P(uint64_t(it.z) | (uint64_t(it.w) << 32));
       }
     } else {
-      const U* ks = static_cast<const U*>(prm.k_in) + row * n;
+      const U* ks = static_cast<const U*>(prm.k_in) + base;
       for (int i = lane; i < n; i += 32) {
         U k = ks[i];
         if (xf.active) k = to_ord<U>(k, xf);
         ka[i] = k;
         if constexpr (Cfg::HAS_P) {
-          P p = static_cast<const P*>(prm.p_in)[row * n + i];
+          P p = static_cast<const P*>(prm.p_in)[base + i];
           if (xf.active) p ^= P(xf.pdesc);
           pa[i] = p;
         }
@@ -390,7 +407,7 @@ __global__ void __launch_bounds__(RssCfg<U, P, NMAX, DAG, MODE, LAYOUT>::WARPS *
 
     // ---- write the row out (coalesced) -------------------------------------
     if constexpr (LAYOUT == LAYOUT_AOS16) {
-      uint4* dst = static_cast<uint4*>(prm.k_out) + row * n;
+      uint4* dst = static_cast<uint4*>(prm.k_out) + base;
       for (int i = lane; i < n; i += 32) {
         const uint64_t k = uint64_t(ka[i]);
         uint64_t p = 0;
@@ -398,7 +415,7 @@ __global__ void __launch_bounds__(RssCfg<U, P, NMAX, DAG, MODE, LAYOUT>::WARPS *
         dst[i] = make_uint4(uint32_t(k), uint32_t(k >> 32), uint32_t(p), uint32_t(p >> 32));
       }
     } else {
-      U* kd = static_cast<U*>(prm.k_out) + row * n;
+      U* kd = static_cast<U*>(prm.k_out) + base;
       for (int i = lane; i < n; i += 32) {
         U k = ka[i];
         if (xf.active) k = from_ord<U>(k, xf);
@@ -406,7 +423,7 @@ __global__ void __launch_bounds__(RssCfg<U, P, NMAX, DAG, MODE, LAYOUT>::WARPS *
         if constexpr (Cfg::HAS_P) {
           P p = pa[i];
           if (xf.active) p ^= P(xf.pdesc);
-          static_cast<P*>(prm.p_out)[row * n + i] = p;
+          static_cast<P*>(prm.p_out)[base + i] = p;
         }
       }
     }
@@ -456,7 +473,9 @@ RssKernel rss_pick(int n, int dag, int key_bytes, int pay, int mode, int layout)
 }
 
 int launch_rss(const nsg_spec& sp, const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows,
-               int64_t n, int key_bytes, int pay, int mode, int layout, const Xform& xf, cudaStream_t st) {
+               int64_t n, int key_bytes, int pay, int mode, int layout, const Xform& xf, cudaStream_t st,
+               const uint32_t* seg_ids = nullptr, const uint32_t* seg_off = nullptr,
+               const uint32_t* seg_count = nullptr, uint32_t* seg_overflow = nullptr) {
   if (n > 1024) return fail(NSG_ERR_SPEC, "RSS rows are limited to 1024 items on the device, got %lld", (long long)n);
   if (sp.kind == NSG_KIND_RSS) {
     if (sp.rss_oversampling < 1 || sp.rss_oversampling > 16)
@@ -483,6 +502,10 @@ int launch_rss(const nsg_spec& sp, const void* k_in, void* k_out, const void* p_
   }
   prm.seed = sp.rss_sample_seed;
   prm.xf = xf;
+  prm.seg_ids = seg_ids;
+  prm.seg_off = seg_off;
+  prm.seg_count = seg_count;
+  prm.seg_overflow = seg_overflow;
   const RssKernel k = rss_pick(int(n), sp.family == 0 ? 0 : 1, key_bytes, pay, mode, layout);
   int dev = 0, sms = 0, occ = 0;
   cudaGetDevice(&dev);
@@ -514,6 +537,21 @@ int launch_rss_rows(const nsg_spec& sp, const void* keys_in, void* keys_out, con
 int launch_rss_items(const nsg_spec& sp, void* rows, int64_t m, int64_t n, cudaStream_t st) {
   if (m <= 0 || n <= 0) return 0;
   return launch_rss(sp, rows, rows, nullptr, nullptr, m, n, 8, 2, MODE_REF, LAYOUT_AOS16, Xform{}, st);
+}
+
+int launch_rss_segment_list(const nsg_spec& sp, const uint32_t* offsets, const uint32_t* ids, const uint32_t* count,
+                            uint32_t* overflow, int64_t max_rows, const void* keys_in, void* keys_out,
+                            const void* pay_in, void* pay_out, cudaStream_t st) {
+  if (max_rows <= 0) return 0;
+  nsg_spec rs = sp;  // long segments: RSS 332 with the spec's network family as base case
+  rs.kind = NSG_KIND_RSS;
+  rs.base_kind = 0;
+  rs.rss_oversampling = 3;
+  rs.rss_block = 2;
+  rs.rss_threshold = 16;
+  rs.rss_sample_seed = 0x5EED;
+  return launch_rss(rs, keys_in, keys_out, pay_in, pay_out, max_rows, 1024, key_bytes_of(sp.key_dtype),
+                    sp.payload_dtype, sp.tie_mode, LAYOUT_SOA, make_xform(sp), st, ids, offsets, count, overflow);
 }
 
 }  // namespace nsg

@@ -5,17 +5,22 @@
 // length", done inside each CTA so the data is read from and written to HBM
 // exactly once:
 //
-//  1. a CTA takes a tile of up to 1024 consecutive segments, stages their
-//     offsets, and copies the tile's contiguous element range into shared
-//     memory (coalesced; ranges larger than the staging buffer are split);
+//  1. a persistent CTA walks tiles of 512 consecutive segments.  The tile's
+//     offsets are prefetched two tiles ahead and its contiguous element range
+//     one tile ahead, with cp.async (16-byte chunks, any element alignment),
+//     into a double-buffered shared-memory ring -- the copy of tile i+1 is in
+//     flight while tile i is binned, sorted and stored;
 //  2. segments are binned by exact length 2..16 with a shared-memory counting
-//     sort, so each warp then runs ONE exact-length network (csrc/gen/nets.cuh)
+//     sort, so each warp runs ONE exact-length network (csrc/gen/nets.cuh)
 //     over 32 segments of (mostly) the same length -- no padding, so REF mode
 //     executes the reference's exact comparator DAG for that length;
-//  3. the tile is written back coalesced;
+//  3. the tile is written back with 16-byte stores (element stores only for
+//     the two partial chunks shared with the neighbouring tiles);
 //  4. segments longer than 16 are appended to a device list and sorted by the
 //     warp Register Sample Sort kernel in a second, stream-ordered launch
 //     (RSS 332 with the spec's network family as base case; <= 1024 items).
+//     Tiles whose element range exceeds the staging buffer are processed in
+//     synchronous sub-tiles.
 #include "common.cuh"
 #include "gen/nets.cuh"
 #include "kernels.cuh"
@@ -25,9 +30,9 @@ namespace nsg {
 
 namespace {
 
-constexpr int kTileSegs = 1024;
+constexpr int kMaxTileSegs = 512;
 constexpr int kThreads = 256;
-constexpr int kDataBytes = 64 * 1024;
+constexpr int kBufBytes = 28 * 1024;  // one staging buffer (keys + payload regions)
 
 struct SegParams {
   const uint32_t* offsets;
@@ -46,25 +51,91 @@ struct SegParams {
 template <class U, class P>
 struct SegGeom {
   static constexpr int PB = PayBytes<P>::value;
-  static constexpr int CAP = kDataBytes / int(sizeof(U) + PB);
-  static constexpr int OFF_OFFS = 0;                                  // (kTileSegs+1) u32
-  static constexpr int OFF_PERM = OFF_OFFS + (kTileSegs + 4) * 4;     // kTileSegs u16
-  static constexpr int OFF_HIST = OFF_PERM + kTileSegs * 2;           // 32 int
-  static constexpr int OFF_CUR = OFF_HIST + 32 * 4;                   // 32 int
-  static constexpr int OFF_KEYS = (OFF_CUR + 32 * 4 + 15) / 16 * 16;  // CAP U
-  static constexpr int OFF_PAYS = OFF_KEYS + CAP * int(sizeof(U));    // CAP P
-  static constexpr int SMEM = OFF_PAYS + CAP * PB;
+  static constexpr int EB = int(sizeof(U)) + PB;
+  static constexpr int CAP = (kBufBytes - 64) / EB / 16 * 16;  // elements per staged (sub)tile
+  // segments per tile: ~CAP/7 keeps the expected element count (mean length
+  // ~5 for the cfg4 distribution) well inside one staging buffer
+  static constexpr int TS = EB <= 8 ? kMaxTileSegs : kMaxTileSegs / 2;
+  static constexpr int K_REG = (CAP * int(sizeof(U)) + 32 + 15) / 16 * 16;
+  static constexpr int P_REG = PB ? (CAP * PB + 32 + 15) / 16 * 16 : 0;
+  static constexpr int BUF = K_REG + P_REG;
+  static constexpr int TS_ = TS;
+  static constexpr int OFFS_STRIDE = TS_ + 4;                    // u32 per offsets slot
+  static constexpr int OFF_OFFS = 0;                                   // 3 slots
+  static constexpr int OFF_PERM = OFF_OFFS + 3 * OFFS_STRIDE * 4;      // TS_ u16
+  static constexpr int OFF_HIST = OFF_PERM + TS_ * 2;            // 32 int
+  static constexpr int OFF_CUR = OFF_HIST + 32 * 4;                    // 32 int
+  static constexpr int OFF_DATA = (OFF_CUR + 32 * 4 + 15) / 16 * 16;   // 2 buffers
+  static constexpr int SMEM = OFF_DATA + 2 * BUF;
 };
 
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+
+// Async copy of elements [e0, e1) (EB bytes each) into `dst` as whole 16-byte
+// chunks; element e lands at dst + shift + (e - e0) * EB with
+// shift = (e0 * EB) % 16.  Never reads past `limit_bytes`.
+template <int EB>
+__device__ __forceinline__ void issue_range(unsigned char* dst, const unsigned char* src, uint32_t e0, uint32_t e1,
+                                            uint64_t limit_bytes, int tid) {
+  const uint64_t c0 = (uint64_t(e0) * EB) >> 4;
+  const uint64_t c1 = (uint64_t(e1) * EB + 15) >> 4;
+  for (uint64_t c = c0 + tid; c < c1; c += kThreads) {
+    const uint64_t g = c << 4;
+    const int64_t rem = int64_t(limit_bytes) - int64_t(g);
+    const int nb = rem >= 16 ? 16 : (rem > 0 ? int(rem) : 0);
+    cp_async16(dst + ((c - c0) << 4), nb ? src + g : src, nb);
+  }
+}
+template <int EB>
+__device__ __forceinline__ int range_shift(uint32_t e0) {
+  return int((uint64_t(e0) * EB) & 15);
+}
+
+// Copy elements [e0, e1) from `sm` (laid out as issue_range left them) back
+// to global: 16-byte stores inside, element stores for the shared edge chunks.
+template <class T>
+__device__ __forceinline__ void store_range(const unsigned char* sm, T* dst, uint32_t e0, uint32_t e1, int tid) {
+  constexpr int EB = int(sizeof(T));
+  const uint64_t b0 = uint64_t(e0) * EB, b1 = uint64_t(e1) * EB;
+  const uint64_t base = b0 & ~uint64_t(15);
+  uint64_t h_end = (b0 + 15) & ~uint64_t(15);
+  if (h_end > b1) h_end = b1;
+  uint64_t t_beg = b1 & ~uint64_t(15);
+  if (t_beg < h_end) t_beg = h_end;
+  unsigned char* g = reinterpret_cast<unsigned char*>(dst);
+  const int nhead = int((h_end - b0) / EB), ntail = int((b1 - t_beg) / EB);
+  if (tid < nhead) {
+    const uint64_t b = b0 + uint64_t(tid) * EB;
+    *reinterpret_cast<T*>(g + b) = *reinterpret_cast<const T*>(sm + (b - base));
+  } else if (tid >= 32 && tid < 32 + ntail) {
+    const uint64_t b = t_beg + uint64_t(tid - 32) * EB;
+    *reinterpret_cast<T*>(g + b) = *reinterpret_cast<const T*>(sm + (b - base));
+  }
+  for (uint64_t c = (h_end >> 4) + tid; c < (t_beg >> 4); c += kThreads) {
+    const uint64_t b = c << 4;
+    stg128_cs(g + b, *reinterpret_cast<const uint4*>(sm + (b - base)));
+  }
+}
+
 template <class U, class P, int DAG, class CX>
-__device__ __forceinline__ void sort_segment_smem(U* keys, P* pays, int st, int len) {
+__device__ __forceinline__ void sort_segment_smem(U* keys, P* pays, int len, const Xform& xf) {
   using E = Elem<U, P>;
+  constexpr bool HAS_P = !IsNoPay<P>::value;
   E v[16];
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
     if (j < len) {
-      v[j].k = keys[st + j];
-      if constexpr (!IsNoPay<P>::value) v[j].p = pays[st + j];
+      U k = keys[j];
+      if (xf.active) k = to_ord<U>(k, xf);
+      v[j].k = k;
+      if constexpr (HAS_P) {
+        P q = pays[j];
+        if (xf.active) q ^= P(xf.pdesc);
+        v[j].p = q;
+      }
     }
   }
   switch (len) {
@@ -88,136 +159,176 @@ __device__ __forceinline__ void sort_segment_smem(U* keys, P* pays, int st, int 
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
     if (j < len) {
-      keys[st + j] = v[j].k;
-      if constexpr (!IsNoPay<P>::value) pays[st + j] = v[j].p;
+      U k = v[j].k;
+      if (xf.active) k = from_ord<U>(k, xf);
+      keys[j] = k;
+      if constexpr (HAS_P) {
+        P q = v[j].p;
+        if (xf.active) q ^= P(xf.pdesc);
+        pays[j] = q;
+      }
     }
   }
 }
 
 template <class U, class P, int MODE, int DAG>
-__global__ void __launch_bounds__(kThreads) seg_kernel(const SegParams prm) {
+__global__ void __launch_bounds__(kThreads, 2) seg_kernel(const SegParams prm) {
   using G = SegGeom<U, P>;
   constexpr bool HAS_P = !IsNoPay<P>::value;
   using CX = typename std::conditional<!HAS_P, CxKeys,
                                        typename std::conditional<MODE == MODE_REF, CxRef, CxUnique>::type>::type;
+  constexpr int TS_ = G::TS;
   extern __shared__ __align__(16) unsigned char sm[];
-  uint32_t* offs = reinterpret_cast<uint32_t*>(sm + G::OFF_OFFS);
   uint16_t* perm = reinterpret_cast<uint16_t*>(sm + G::OFF_PERM);
   int* hist = reinterpret_cast<int*>(sm + G::OFF_HIST);
   int* cur = reinterpret_cast<int*>(sm + G::OFF_CUR);
-  U* keys = reinterpret_cast<U*>(sm + G::OFF_KEYS);
-  P* pays = reinterpret_cast<P*>(sm + G::OFF_PAYS);
   const int tid = threadIdx.x;
   const Xform xf = prm.xf;
-  const U* kin = static_cast<const U*>(prm.k_in);
+  const unsigned char* kin = static_cast<const unsigned char*>(prm.k_in);
+  const unsigned char* pin = static_cast<const unsigned char*>(prm.p_in);
   U* kout = static_cast<U*>(prm.k_out);
-  const P* pin = static_cast<const P*>(prm.p_in);
   P* pout = static_cast<P*>(prm.p_out);
-  const int64_t ntiles = (prm.nseg + kTileSegs - 1) / kTileSegs;
+  const int64_t ntiles = (prm.nseg + TS_ - 1) / TS_;
+  const int64_t gstride = gridDim.x;
+  const uint32_t total = prm.offsets[prm.nseg];
+  const uint64_t klimit = uint64_t(total) * sizeof(U), plimit = uint64_t(total) * G::PB;
 
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t s_begin = tile * kTileSegs;
-    const int nts = int(prm.nseg - s_begin < kTileSegs ? prm.nseg - s_begin : kTileSegs);
+  auto offs_slot = [&](int64_t k) { return reinterpret_cast<uint32_t*>(sm + G::OFF_OFFS) + (k % 3) * G::OFFS_STRIDE; };
+  auto data_slot = [&](int64_t k) { return sm + G::OFF_DATA + (k & 1) * G::BUF; };
+  auto nsegs_of = [&](int64_t t) { return int(prm.nseg - t * TS_ < TS_ ? prm.nseg - t * TS_ : TS_); };
+  auto issue_offs = [&](int64_t t, uint32_t* dst) {
+    const int nts = nsegs_of(t);
+    for (int i = tid; i <= nts; i += kThreads) cp_async4(dst + i, prm.offsets + t * TS_ + i);
+  };
+  auto issue_data = [&](unsigned char* buf, uint32_t e0, uint32_t e1) {
+    issue_range<int(sizeof(U))>(buf, kin, e0, e1, klimit, tid);
+    if constexpr (HAS_P) issue_range<G::PB>(buf + G::K_REG, pin, e0, e1, plimit, tid);
+  };
+
+  // Bin + sort + store the segments [a, b) of a tile whose elements
+  // [offs[a], offs[b]) are staged in `buf` (or, if !staged, only collect longs).
+  auto process = [&](const uint32_t* offs, int a, int b, int64_t seg0, unsigned char* buf, bool staged) {
+    const uint32_t e0 = offs[a], e1 = offs[b];
+    unsigned char* kb = buf + range_shift<int(sizeof(U))>(e0);
+    unsigned char* pb = buf + G::K_REG + (HAS_P ? range_shift<G::PB>(e0) : 0);
+    if (tid < 32) hist[tid] = 0;
     __syncthreads();
-    for (int i = tid; i <= nts; i += kThreads) offs[i] = prm.offsets[s_begin + i];
+    for (int s = a + tid; s < b; s += kThreads) {
+      const int len = int(offs[s + 1] - offs[s]);
+      if (len > 16) {
+        const uint32_t slot = atomicAdd(prm.long_count, 1u);
+        if (slot < prm.long_cap)
+          prm.long_ids[slot] = uint32_t(seg0 + s);
+        else
+          atomicAdd(prm.overflow, 1u);
+      } else if (len >= 2) {
+        atomicAdd(&hist[len], 1);
+      }
+    }
     __syncthreads();
+    if (tid < 32) {  // exclusive scan over the length bins
+      const int v = hist[tid];
+      int incl = v;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, d);
+        if (tid >= d) incl += t;
+      }
+      cur[tid] = incl - v;
+      if (tid == 31) hist[31] = incl;
+    }
+    __syncthreads();
+    const int nshort = hist[31];
+    for (int s = a + tid; s < b; s += kThreads) {
+      const int len = int(offs[s + 1] - offs[s]);
+      if (len >= 2 && len <= 16) perm[atomicAdd(&cur[len], 1)] = uint16_t(s - a);
+    }
+    __syncthreads();
+    if (staged) {
+      for (int j = tid; j < nshort; j += kThreads) {
+        const int s = a + perm[j];
+        const int st = int(offs[s] - e0);
+        sort_segment_smem<U, P, DAG, CX>(reinterpret_cast<U*>(kb) + st, reinterpret_cast<P*>(pb) + st,
+                                         int(offs[s + 1] - offs[s]), xf);
+      }
+      __syncthreads();
+      store_range<U>(buf, kout, e0, e1, tid);
+      if constexpr (HAS_P) store_range<P>(buf + G::K_REG, pout, e0, e1, tid);
+    }
+    __syncthreads();
+  };
+
+  int64_t t = blockIdx.x;
+  if (t >= ntiles) return;
+  // prologue: offsets of tile 0 (synchronously), data of tile 0 + offsets of tile 1 (async)
+  issue_offs(t, offs_slot(0));
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  {
+    const uint32_t* o = offs_slot(0);
+    const int nts = nsegs_of(t);
+    if (o[nts] - o[0] <= uint32_t(G::CAP)) issue_data(data_slot(0), o[0], o[nts]);
+    if (t + gstride < ntiles) issue_offs(t + gstride, offs_slot(1));
+    cp_async_commit();
+  }
+  for (int64_t k = 0; t < ntiles; ++k, t += gstride) {
+    cp_async_wait<0>();
+    __syncthreads();
+    const uint32_t* offs = offs_slot(k);
+    const int nts = nsegs_of(t);
+    const bool fits = offs[nts] - offs[0] <= uint32_t(G::CAP);
+    const int64_t tn = t + gstride;
+    if (tn < ntiles) {  // prefetch: data of the next tile, offsets of the one after
+      const uint32_t* on = offs_slot(k + 1);
+      const int ntn = nsegs_of(tn);
+      if (on[ntn] - on[0] <= uint32_t(G::CAP)) issue_data(data_slot(k + 1), on[0], on[ntn]);
+      if (tn + gstride < ntiles) issue_offs(tn + gstride, offs_slot(k + 2));
+    }
+    cp_async_commit();
+    unsigned char* buf = data_slot(k);
+    // a fitting tile is one prefetched sub-tile; an oversized one is cut into
+    // synchronous sub-tiles of <= CAP elements (one call site keeps `process`
+    // inlined, so the per-thread network stays in registers)
     int a = 0;
     while (a < nts) {
-      // largest b with offs[b] - offs[a] <= CAP (at least a + 1)
-      int b;
-      const uint32_t e0 = offs[a];
-      if (offs[a + 1] - e0 > uint32_t(G::CAP)) {
-        b = a + 1;
-      } else {
-        int lo = a + 1, hi = nts;
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (offs[mid] - e0 <= uint32_t(G::CAP)) lo = mid; else hi = mid - 1;
-        }
-        b = lo;
-      }
-      const int ne = int(offs[b] - e0);
-      const bool staged = ne <= G::CAP;
-      if (staged) {
-#pragma unroll 4
-        for (int i = tid; i < ne; i += kThreads) {
-          U k = kin[int64_t(e0) + i];
-          if (xf.active) k = to_ord<U>(k, xf);
-          keys[i] = k;
-          if constexpr (HAS_P) {
-            P q = pin[int64_t(e0) + i];
-            if (xf.active) q ^= P(xf.pdesc);
-            pays[i] = q;
+      int b = nts;
+      bool staged = true;
+      if (!fits) {
+        if (offs[a + 1] - offs[a] > uint32_t(G::CAP)) {
+          b = a + 1;  // one long segment: listed for the RSS pass, not staged
+        } else {
+          int lo = a + 1, hi = nts;
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (offs[mid] - offs[a] <= uint32_t(G::CAP)) lo = mid; else hi = mid - 1;
           }
+          b = lo;
+        }
+        staged = offs[b] - offs[a] <= uint32_t(G::CAP);
+        if (staged) {
+          issue_data(buf, offs[a], offs[b]);
+          cp_async_commit();
+          cp_async_wait<0>();
+          __syncthreads();
         }
       }
-      if (tid < 32) hist[tid] = 0;
-      __syncthreads();
-      for (int s = a + tid; s < b; s += kThreads) {
-        const int len = int(offs[s + 1] - offs[s]);
-        if (len > 16) {
-          const uint32_t slot = atomicAdd(prm.long_count, 1u);
-          if (slot < prm.long_cap)
-            prm.long_ids[slot] = uint32_t(s_begin + s);
-          else
-            atomicAdd(prm.overflow, 1u);
-        } else if (len >= 2) {
-          atomicAdd(&hist[len], 1);
-        }
-      }
-      __syncthreads();
-      if (tid < 32) {  // exclusive scan of the 17 bins
-        const int v = hist[tid];
-        int incl = v;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const int t = __shfl_up_sync(0xffffffffu, incl, d);
-          if (tid >= d) incl += t;
-        }
-        cur[tid] = incl - v;
-        if (tid == 31) hist[31] = incl;  // total short segments (bins 17..30 are 0)
-      }
-      __syncthreads();
-      const int nshort = hist[31];
-      for (int s = a + tid; s < b; s += kThreads) {
-        const int len = int(offs[s + 1] - offs[s]);
-        if (len >= 2 && len <= 16) perm[atomicAdd(&cur[len], 1)] = uint16_t(s - a);
-      }
-      __syncthreads();
-      if (staged) {
-        for (int j = tid; j < nshort; j += kThreads) {
-          const int s = a + perm[j];
-          sort_segment_smem<U, P, DAG, CX>(keys, pays, int(offs[s] - e0), int(offs[s + 1] - offs[s]));
-        }
-      }
-      __syncthreads();
-      if (staged) {
-#pragma unroll 4
-        for (int i = tid; i < ne; i += kThreads) {
-          U k = keys[i];
-          if (xf.active) k = from_ord<U>(k, xf);
-          kout[int64_t(e0) + i] = k;
-          if constexpr (HAS_P) {
-            P q = pays[i];
-            if (xf.active) q ^= P(xf.pdesc);
-            pout[int64_t(e0) + i] = q;
-          }
-        }
-      }
-      __syncthreads();
+      process(offs, a, b, t * TS_, buf, staged);
       a = b;
     }
   }
+  cp_async_wait<0>();
 }
 
 struct SegKernel {
   const void* fn;
   int smem;
+  int ts;
 };
 
 template <class U, class P, int MODE, int DAG>
 SegKernel seg_info() {
-  return {reinterpret_cast<const void*>(&seg_kernel<U, P, MODE, DAG>), SegGeom<U, P>::SMEM};
+  return {reinterpret_cast<const void*>(&seg_kernel<U, P, MODE, DAG>), SegGeom<U, P>::SMEM, SegGeom<U, P>::TS};
 }
 
 template <int DAG>
@@ -244,6 +355,7 @@ size_t segments_ws_bytes(int64_t nseg, int64_t nelem) {
 int launch_segments(const nsg_spec& sp, const uint32_t* offsets, int64_t nseg, const void* keys_in, void* keys_out,
                     const void* pay_in, void* pay_out, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (nseg <= 0) return 0;
+  if (nseg >= (int64_t(1) << 32)) return fail(NSG_ERR_SPEC, "segment count must fit in uint32");
   if (ws_bytes < 16 || !ws) return fail(NSG_ERR_SPEC, "segmented sort needs a workspace (nsg_segments_ws_bytes)");
   uint32_t* w = static_cast<uint32_t*>(ws);
   const uint32_t cap = uint32_t((ws_bytes - 16) / 4);
@@ -260,7 +372,7 @@ int launch_segments(const nsg_spec& sp, const uint32_t* offsets, int64_t nseg, c
   cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, k.smem);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k.fn, kThreads, k.smem);
   if (occ < 1) return fail(NSG_ERR_CUDA, "segment kernel cannot be resident");
-  const int64_t ntiles = (nseg + kTileSegs - 1) / kTileSegs;
+  const int64_t ntiles = (nseg + k.ts - 1) / k.ts;
   const int64_t grid = ntiles < int64_t(sms) * occ ? ntiles : int64_t(sms) * occ;
   void* args[] = {&prm};
   e = cudaLaunchKernel(k.fn, dim3(unsigned(grid)), dim3(kThreads), args, size_t(k.smem), st);

@@ -32,7 +32,10 @@ extern "C" {
 #define NSG_ERR_CUDA (-3)
 
 /* kinds / families / tie modes: reference registry.py:24, networks.py:30 */
-enum { NSG_KIND_NETWORK = 0, NSG_KIND_INSERTION = 1, NSG_KIND_RSS = 2, NSG_KIND_HYBRID = 3, NSG_KIND_STD = 4 };
+enum { NSG_KIND_NETWORK = 0, NSG_KIND_INSERTION = 1, NSG_KIND_RSS = 2, NSG_KIND_HYBRID = 3, NSG_KIND_STD = 4,
+       /* extension: merge sorter for n > 16 (odd-even merge network at 32/64,
+          warp bitonic merge otherwise); keys-only or UNIQUE mode */
+       NSG_KIND_MERGE = 5 };
 enum { NSG_KEY_U32 = 0, NSG_KEY_U64 = 1, NSG_KEY_I32 = 2, NSG_KEY_I64 = 3, NSG_KEY_F32 = 4, NSG_KEY_F64 = 5 };
 enum { NSG_PAY_NONE = 0, NSG_PAY_U32 = 1, NSG_PAY_U64 = 2 };
 enum { NSG_TIE_REF = 0, NSG_TIE_UNIQUE = 1 };

@@ -58,6 +58,8 @@ def make_row_spec(kind: str, family: str, swap: str, rss_cfg: str, rss_base: str
         return registry.spec_rss(rss_cfg, rss_base)
     if kind == "insertion":
         return registry.spec_insertion("Def")
+    if kind == "merge":
+        return registry.spec_merge(family)
     raise ConfigurationError(f"unknown kind {kind!r}")
 
 

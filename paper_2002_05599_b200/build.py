@@ -28,8 +28,8 @@ FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--
 
 def _units() -> list:
     """(object name, source, extra defines)"""
-    units = [("net_n%02d.o" % n, CSRC / "net_sort_inst.cu", ["-DNSG_N=%d" % n]) for n in range(1, 17)]
-    for name in ("capi", "misc", "rss", "segments"):
+    units = [("net_n%02d.o" % n, CSRC / "net_sort_inst.cu", ["-DNSG_N=%d" % n]) for n in list(range(1, 17)) + [32, 64]]
+    for name in ("capi", "misc", "rss", "segments", "wmerge"):
         units.append((name + ".o", CSRC / (name + ".cu"), []))
     return units
 

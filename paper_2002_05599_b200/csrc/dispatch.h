@@ -31,6 +31,8 @@ NSG_DECLARE_NET_LOOKUP(13)
 NSG_DECLARE_NET_LOOKUP(14)
 NSG_DECLARE_NET_LOOKUP(15)
 NSG_DECLARE_NET_LOOKUP(16)
+NSG_DECLARE_NET_LOOKUP(32)
+NSG_DECLARE_NET_LOOKUP(64)
 #undef NSG_DECLARE_NET_LOOKUP
 
 KernelInfo net_lookup(int n, int dag, int key_bytes, int pay, int mode, int layout);

@@ -28,6 +28,10 @@ int launch_rss_segment_list(const nsg_spec& sp, const uint32_t* offsets, const u
                             uint32_t* overflow, int64_t max_rows, const void* keys_in, void* keys_out,
                             const void* pay_in, void* pay_out, cudaStream_t st);
 
+// wmerge.cu
+int launch_wmerge(const nsg_spec& sp, const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows,
+                  int64_t n, cudaStream_t st);
+
 // segments.cu
 size_t segments_ws_bytes(int64_t nseg, int64_t nelem);
 int launch_segments(const nsg_spec& sp, const uint32_t* offsets, int64_t nseg, const void* keys_in, void* keys_out,

@@ -40,19 +40,31 @@ struct NetParams {
 };
 
 // Shared-memory geometry of one region (keys, payloads, or AoS items).
+//  * rows of an odd number S of 16-byte chunks (or not 16-byte multiples):
+//    plain layout, lane stride is odd in vector units -> conflict-free;
+//  * S a power of two >= 2: XOR swizzle  phys = q ^ ((q / S) & 7)  on the
+//    16-byte chunk index q -- a bijection that keeps both the linear tile copy
+//    (8 consecutive chunks per quarter-warp) and the per-lane row reads
+//    (8 rows, same chunk) on 8 distinct bank groups, with no padding;
+//  * other even S: pad each row by 16 bytes (odd stride).
 template <int N, int EB>
 struct RowGeom {
   static constexpr int R = N * EB;  // row bytes in HBM
   static constexpr int V = (R % 16 == 0) ? 16 : ((R % 8 == 0) ? 8 : 4);
-  static constexpr bool PAD = (V == 16) && ((R / 16) % 2 == 0);
+  static constexpr int S = R / 16;
+  static constexpr bool SWZ = (V == 16) && S >= 2 && (S & (S - 1)) == 0;
+  static constexpr bool PAD = (V == 16) && (S % 2 == 0) && !SWZ;
   static constexpr int RS = R + (PAD ? 16 : 0);  // row stride in smem
   static constexpr int W = R / 4;                // 32-bit words per row
+
+  __device__ __forceinline__ static int swz(int q) { return q ^ ((q / S) & 7); }
 
   // smem byte offset of the 16-byte chunk q of the contiguous tile
   __device__ __forceinline__ static int chunk_off(int q) {
     if constexpr (PAD) {
-      constexpr int C = R / 16;
-      return (q / C) * RS + (q % C) * 16;
+      return (q / S) * RS + (q % S) * 16;
+    } else if constexpr (SWZ) {
+      return swz(q) * 16;
     } else {
       return q * 16;
     }
@@ -62,7 +74,10 @@ struct RowGeom {
     const unsigned char* rp = base + r * RS;
 #pragma unroll
     for (int i = 0; i < R / V; ++i) {
-      if constexpr (V == 16) {
+      if constexpr (SWZ) {
+        const uint4 x = *reinterpret_cast<const uint4*>(base + swz(r * S + i) * 16);
+        w[4 * i] = x.x; w[4 * i + 1] = x.y; w[4 * i + 2] = x.z; w[4 * i + 3] = x.w;
+      } else if constexpr (V == 16) {
         const uint4 x = *reinterpret_cast<const uint4*>(rp + 16 * i);
         w[4 * i] = x.x; w[4 * i + 1] = x.y; w[4 * i + 2] = x.z; w[4 * i + 3] = x.w;
       } else if constexpr (V == 8) {
@@ -78,7 +93,10 @@ struct RowGeom {
     unsigned char* rp = base + r * RS;
 #pragma unroll
     for (int i = 0; i < R / V; ++i) {
-      if constexpr (V == 16) {
+      if constexpr (SWZ) {
+        *reinterpret_cast<uint4*>(base + swz(r * S + i) * 16) =
+            make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+      } else if constexpr (V == 16) {
         *reinterpret_cast<uint4*>(rp + 16 * i) = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
       } else if constexpr (V == 8) {
         *reinterpret_cast<uint2*>(rp + 8 * i) = make_uint2(w[2 * i], w[2 * i + 1]);
@@ -192,6 +210,83 @@ __device__ __forceinline__ void store_region(const unsigned char* sm, unsigned c
 }
 
 // ---- per-lane row sort ----------------------------------------------------
+// Three phases over the lane's APL rows (all loads, all networks, all stores)
+// so the shared-memory loads of every row are in flight together: a store of
+// row a may alias a load of row a+1 as far as the compiler knows, so a fused
+// per-row loop would serialise LDS latency behind each network.
+template <class Cfg>
+__device__ __forceinline__ void load_row_elems(const unsigned char* smk, const unsigned char* smp, int r,
+                                               Elem<typename Cfg::U, typename Cfg::P> (&e)[Cfg::N]) {
+  using U = typename Cfg::U;
+  using P = typename Cfg::P;
+  constexpr int N = Cfg::N;
+  uint32_t wk[Cfg::GK::W];
+  Cfg::GK::load_row(smk, r, wk);
+  if constexpr (Cfg::LAYOUT == LAYOUT_AOS16) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      e[j].k = word_get<uint64_t>(wk, 2 * j);
+      e[j].p = word_get<uint64_t>(wk, 2 * j + 1);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < N; ++j) e[j].k = word_get<U>(wk, j);
+    if constexpr (Cfg::HAS_P) {
+      uint32_t wp[Cfg::GP::W];
+      Cfg::GP::load_row(smp, r, wp);
+#pragma unroll
+      for (int j = 0; j < N; ++j) e[j].p = word_get<P>(wp, j);
+    }
+  }
+}
+
+template <class Cfg>
+__device__ __forceinline__ void sort_elems(Elem<typename Cfg::U, typename Cfg::P> (&e)[Cfg::N], const Xform& xf) {
+  using U = typename Cfg::U;
+  using P = typename Cfg::P;
+  constexpr int N = Cfg::N;
+  if (xf.active) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      e[j].k = to_ord<U>(e[j].k, xf);
+      if constexpr (Cfg::HAS_P) e[j].p ^= P(xf.pdesc);
+    }
+  }
+  Net<Cfg::DAG, N>::template run<typename Cfg::CX>(e);
+  if (xf.active) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      e[j].k = from_ord<U>(e[j].k, xf);
+      if constexpr (Cfg::HAS_P) e[j].p ^= P(xf.pdesc);
+    }
+  }
+}
+
+template <class Cfg>
+__device__ __forceinline__ void store_row_elems(unsigned char* smk, unsigned char* smp, int r,
+                                                const Elem<typename Cfg::U, typename Cfg::P> (&e)[Cfg::N]) {
+  constexpr int N = Cfg::N;
+  uint32_t wk[Cfg::GK::W];
+  if constexpr (Cfg::LAYOUT == LAYOUT_AOS16) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      word_put(wk, 2 * j, e[j].k);
+      word_put(wk, 2 * j + 1, e[j].p);
+    }
+    Cfg::GK::store_row(smk, r, wk);
+  } else {
+#pragma unroll
+    for (int j = 0; j < N; ++j) word_put(wk, j, e[j].k);
+    Cfg::GK::store_row(smk, r, wk);
+    if constexpr (Cfg::HAS_P) {
+      uint32_t wp[Cfg::GP::W];
+#pragma unroll
+      for (int j = 0; j < N; ++j) word_put(wp, j, e[j].p);
+      Cfg::GP::store_row(smp, r, wp);
+    }
+  }
+}
+
 template <class Cfg>
 __device__ __forceinline__ void sort_row(unsigned char* smk, unsigned char* smp, int r, const Xform& xf) {
   using U = typename Cfg::U;
@@ -296,10 +391,18 @@ __global__ void __launch_bounds__(Cfg::WARPS * 32) net_sort_kernel(const NetPara
     unsigned char* smp = smk + Cfg::K_SMEM;
     const int64_t row0 = t * ROWS;
     const int vrows = p.rows - row0 < ROWS ? int(p.rows - row0) : ROWS;
+    if constexpr (Cfg::APL == 1) {
+      if (lane < vrows) sort_row<Cfg>(smk, smp, lane, p.xf);
+    } else {
+      Elem<typename Cfg::U, typename Cfg::P> e[Cfg::APL][Cfg::N];
 #pragma unroll
-    for (int a = 0; a < Cfg::APL; ++a) {
-      const int r = a * 32 + lane;
-      if (r < vrows) sort_row<Cfg>(smk, smp, r, p.xf);
+      for (int a = 0; a < Cfg::APL; ++a)
+        if (a * 32 + lane < vrows) load_row_elems<Cfg>(smk, smp, a * 32 + lane, e[a]);
+#pragma unroll
+      for (int a = 0; a < Cfg::APL; ++a) sort_elems<Cfg>(e[a], p.xf);
+#pragma unroll
+      for (int a = 0; a < Cfg::APL; ++a)
+        if (a * 32 + lane < vrows) store_row_elems<Cfg>(smk, smp, a * 32 + lane, e[a]);
     }
     __syncwarp();
     store_region<typename Cfg::GK, ROWS>(smk, kout + row0 * Cfg::GK::R, vrows * Cfg::GK::R, lane);

@@ -47,9 +47,24 @@ KernelInfo lookup_dag(int key_bytes, int pay, int mode, int layout) {
 
 #define NSG_CAT2(a, b) a##b
 #define NSG_CAT(a, b) NSG_CAT2(a, b)
+#if NSG_N > 16
+// 32 / 64 items: the odd-even merge network (DAG 2), keys-only or UNIQUE payload
+KernelInfo NSG_CAT(net_lookup_n, NSG_N)(int dag, int key_bytes, int pay, int mode, int layout) {
+  if (dag != 2 || layout != LAYOUT_SOA || (pay != 0 && mode != MODE_UNIQUE)) return KernelInfo{};
+  if (key_bytes == 4) {
+    if (pay == 0) return info<NSG_N, 2, uint32_t, NoPay, MODE_UNIQUE, LAYOUT_SOA>();
+    if (pay == 1) return info<NSG_N, 2, uint32_t, uint32_t, MODE_UNIQUE, LAYOUT_SOA>();
+    return info<NSG_N, 2, uint32_t, uint64_t, MODE_UNIQUE, LAYOUT_SOA>();
+  }
+  if (pay == 0) return info<NSG_N, 2, uint64_t, NoPay, MODE_UNIQUE, LAYOUT_SOA>();
+  if (pay == 1) return info<NSG_N, 2, uint64_t, uint32_t, MODE_UNIQUE, LAYOUT_SOA>();
+  return info<NSG_N, 2, uint64_t, uint64_t, MODE_UNIQUE, LAYOUT_SOA>();
+}
+#else
 KernelInfo NSG_CAT(net_lookup_n, NSG_N)(int dag, int key_bytes, int pay, int mode, int layout) {
   return dag ? lookup_dag<NSG_N, 1>(key_bytes, pay, mode, layout)
              : lookup_dag<NSG_N, 0>(key_bytes, pay, mode, layout);
 }
+#endif
 
 }  // namespace nsg

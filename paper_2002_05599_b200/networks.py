@@ -247,5 +247,45 @@ def verify_zero_one(net: Network) -> bool:
 
 def dag_comparators(dag: int, n: int) -> tuple:
     """Comparator list the device compiles for (dag, n), level-scheduled."""
-    net = best_network(n) if dag == DAG_BEST else generate_bose_nelson(n)
+    if dag == DAG_MERGE:
+        net = merge_network(n)
+    else:
+        net = best_network(n) if dag == DAG_BEST else generate_bose_nelson(n)
     return tuple(c for level in compute_levels(net) for c in level)
+
+
+# ---------------------------------------------------------------------------
+# Merge networks for 32 / 64 items (the device's thread-per-array "merge"
+# sorter; no counterpart in the reference, which switches to RSS above 16)
+# ---------------------------------------------------------------------------
+
+DAG_MERGE = 2
+
+
+def _odd_even_merge(lo: int, n: int, r: int, out: list) -> None:
+    """Batcher's odd-even merge of the two sorted halves of a[lo:lo+n] (stride r)."""
+    step = 2 * r
+    if step < n:
+        _odd_even_merge(lo, n, step, out)
+        _odd_even_merge(lo + r, n, step, out)
+        for i in range(lo + r, lo + n - r, step):
+            out.append(Comparator(i, i + r))
+    else:
+        out.append(Comparator(lo, lo + r))
+
+
+@functools.lru_cache(maxsize=None)
+def merge_network(n: int) -> Network:
+    """n = 32 / 64: two sorted halves (Green-16 at the bottom) + odd-even merge.
+
+    32 items: 2 x 60 + 65 = 185 comparators (the best known size), depth 15.
+    """
+    if n == 16:
+        return best_network(16)
+    if n not in (32, 64):
+        raise UnsupportedSize(f"merge networks are built for 32 and 64 items, got {n}")
+    half = merge_network(n // 2)
+    comps = list(half.comparators)
+    comps += [Comparator(a + n // 2, b + n // 2) for a, b in half.comparators]
+    _odd_even_merge(0, n, 1, comps)
+    return Network(n, tuple(comps), "OddEvenMerge")

@@ -94,9 +94,11 @@ def main():
             rev = torch.flip(srt, dims=[1]).contiguous()
             ot = torch.empty_like(uni)
             for dname, x in (("uniform", uni), ("few16", few), ("sorted", srt), ("reverse", rev)):
-                med, best = timeit(torch, lambda: batch.sort_rows(x, kind="rss", out_keys=ot), a.reps)
-                assert torch.equal(ot, torch.sort(x, dim=1).values)
-                report(f"cfg3 RSS 332 2^20 x n={n} i64 {dname}", 2 * rows * n * 8, rows, med, best)
+                for kind in ("rss", "merge"):
+                    med, best = timeit(torch, lambda: batch.sort_rows(x, kind=kind, out_keys=ot), a.reps)
+                    assert torch.equal(ot, torch.sort(x, dim=1).values)
+                    label = "RSS 332" if kind == "rss" else "merge"
+                    report(f"cfg3 {label} 2^20 x n={n} i64 {dname}", 2 * rows * n * 8, rows, med, best)
             del uni, few, srt, rev, ot
             torch.cuda.empty_cache()
 

@@ -19,6 +19,8 @@ from pathlib import Path
 from .errors import ConfigurationError, CorrectnessFailure, DeviceError, UnsupportedSize
 
 LIB_PATH = Path(__file__).resolve().parent / "libnsg.so"
+if os.environ.get("NSG_LIB_PATH"):  # tuning variants only (tools/variants.py)
+    LIB_PATH = Path(os.environ["NSG_LIB_PATH"]).resolve()
 
 NSG_OK, NSG_ERR_CHECK, NSG_ERR_SPEC, NSG_ERR_CUDA = 0, -1, -2, -3
 

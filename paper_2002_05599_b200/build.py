@@ -46,10 +46,15 @@ def _stale(target: Path, deps: list) -> bool:
     return any(d.stat().st_mtime > t for d in deps if d.exists())
 
 
-def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -> Path:
+def build(force: bool = False, jobs: int | None = None, verbose: bool = False, defines: tuple = (),
+          lib_path: Path | None = None, obj_dir: Path | None = None) -> Path:
+    """Build libnsg.so.  `defines` / `lib_path` / `obj_dir` build tuning
+    variants (tools/variants.py) next to, never instead of, the product."""
     subprocess.run([sys.executable, str(ROOT / "tools" / "gen_networks.py")], check=True,
                    stdout=None if verbose else subprocess.DEVNULL)
-    OBJ.mkdir(exist_ok=True)
+    OBJ = Path(obj_dir) if obj_dir else globals()["OBJ"]
+    LIB = Path(lib_path) if lib_path else globals()["LIB"]
+    OBJ.mkdir(parents=True, exist_ok=True)
     headers = _headers()
     todo = []
     for obj, src, extra in _units():
@@ -59,7 +64,7 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -
 
     def compile_one(item):
         out, src, extra = item
-        cmd = [NVCC] + FLAGS + extra + ["-c", str(src), "-o", str(out)]
+        cmd = [NVCC] + FLAGS + [f"-D{d}" for d in defines] + extra + ["-c", str(src), "-o", str(out)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src.name} {extra}:\n{r.stderr}")

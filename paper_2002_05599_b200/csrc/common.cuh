@@ -172,11 +172,19 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-// Streaming 16-byte global store (output is not re-read by this kernel).
+// 16-byte global store; streaming (.cs, evict-first) by default since the
+// output is not re-read by this kernel.  NSG_STG_CS=0 selects a plain store.
+#ifndef NSG_STG_CS
+#define NSG_STG_CS 1
+#endif
 __device__ __forceinline__ void stg128_cs(void* g, uint4 v) {
+#if NSG_STG_CS
   asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};\n" ::"l"(g), "r"(v.x), "r"(v.y), "r"(v.z),
                "r"(v.w)
                : "memory");
+#else
+  *reinterpret_cast<uint4*>(g) = v;
+#endif
 }
 
 }  // namespace nsg

@@ -25,6 +25,17 @@
 #include "common.cuh"
 #include "gen/nets.cuh"
 
+// Tuning knobs (compile-time; tools/variants.py sweeps them).
+#ifndef NSG_TILE_BYTES
+#define NSG_TILE_BYTES 4096
+#endif
+#ifndef NSG_STAGES
+#define NSG_STAGES 3
+#endif
+#ifndef NSG_WARPS
+#define NSG_WARPS 4
+#endif
+
 namespace nsg {
 
 enum Mode { MODE_REF = 0, MODE_UNIQUE = 1 };
@@ -138,15 +149,18 @@ struct NetCfg {
   using GK = RowGeom<N, KEB>;
   using GP = RowGeom<N, (PEB ? PEB : 4)>;
   static constexpr int ROW_BYTES = GK::R + (PEB ? GP::R : 0);
-  // ~4 KiB of HBM bytes per warp per stage
-  static constexpr int APL_RAW = 4096 / (32 * ROW_BYTES);
+  // ~NSG_TILE_BYTES of HBM bytes per warp per stage
+  static constexpr int APL_RAW = NSG_TILE_BYTES / (32 * ROW_BYTES);
   static constexpr int APL = APL_RAW >= 16 ? 16 : APL_RAW >= 8 ? 8 : APL_RAW >= 4 ? 4 : APL_RAW >= 2 ? 2 : 1;
   static constexpr int ROWS = 32 * APL;
-  static constexpr int STAGES = 3;
   static constexpr int K_SMEM = ROWS * GK::RS;
   static constexpr int P_SMEM = PEB ? ROWS * GP::RS : 0;
   static constexpr int STAGE_SMEM = K_SMEM + P_SMEM;
-  static constexpr int WARPS = 4;
+  // ring depth and warps per CTA shrink for very long rows (n = 32 / 64)
+  static constexpr int SMEM_BUDGET = 200 * 1024;
+  static constexpr int STAGES = (NSG_STAGES * STAGE_SMEM <= SMEM_BUDGET / 2) ? NSG_STAGES : 2;
+  static constexpr int WARPS_FIT = SMEM_BUDGET / (STAGES * STAGE_SMEM);
+  static constexpr int WARPS = WARPS_FIT >= NSG_WARPS ? NSG_WARPS : (WARPS_FIT >= 1 ? WARPS_FIT : 1);
   static constexpr int WARP_SMEM = STAGES * STAGE_SMEM;
   static constexpr int CTA_SMEM = WARPS * WARP_SMEM;
   using CX = typename std::conditional<!HAS_P, CxKeys,

@@ -30,9 +30,11 @@ namespace nsg {
 
 namespace {
 
-constexpr int kMaxTileSegs = 512;
-constexpr int kThreads = 256;
-constexpr int kBufBytes = 28 * 1024;  // one staging buffer (keys + payload regions)
+// 128-thread CTAs with ~45 KB of shared memory: 4-5 CTAs per SM, so one
+// CTA's barrier waits are covered by the others
+constexpr int kMaxTileSegs = 256;
+constexpr int kThreads = 128;
+constexpr int kBufBytes = 20 * 1024;  // one staging buffer (keys + payload regions)
 
 struct SegParams {
   const uint32_t* offsets;
@@ -96,8 +98,10 @@ __device__ __forceinline__ int range_shift(uint32_t e0) {
 
 // Copy elements [e0, e1) from `sm` (laid out as issue_range left them) back
 // to global: 16-byte stores inside, element stores for the shared edge chunks.
-template <class T>
-__device__ __forceinline__ void store_range(const unsigned char* sm, T* dst, uint32_t e0, uint32_t e1, int tid) {
+// `f` maps each element back from the ordered space (identity when inactive).
+template <class T, class F>
+__device__ __forceinline__ void store_range(const unsigned char* sm, T* dst, uint32_t e0, uint32_t e1, int tid,
+                                            F f) {
   constexpr int EB = int(sizeof(T));
   const uint64_t b0 = uint64_t(e0) * EB, b1 = uint64_t(e1) * EB;
   const uint64_t base = b0 & ~uint64_t(15);
@@ -109,70 +113,69 @@ __device__ __forceinline__ void store_range(const unsigned char* sm, T* dst, uin
   const int nhead = int((h_end - b0) / EB), ntail = int((b1 - t_beg) / EB);
   if (tid < nhead) {
     const uint64_t b = b0 + uint64_t(tid) * EB;
-    *reinterpret_cast<T*>(g + b) = *reinterpret_cast<const T*>(sm + (b - base));
+    *reinterpret_cast<T*>(g + b) = f(*reinterpret_cast<const T*>(sm + (b - base)));
   } else if (tid >= 32 && tid < 32 + ntail) {
     const uint64_t b = t_beg + uint64_t(tid - 32) * EB;
-    *reinterpret_cast<T*>(g + b) = *reinterpret_cast<const T*>(sm + (b - base));
+    *reinterpret_cast<T*>(g + b) = f(*reinterpret_cast<const T*>(sm + (b - base)));
   }
   for (uint64_t c = (h_end >> 4) + tid; c < (t_beg >> 4); c += kThreads) {
     const uint64_t b = c << 4;
-    stg128_cs(g + b, *reinterpret_cast<const uint4*>(sm + (b - base)));
+    union {
+      uint4 v;
+      T e[16 / EB];
+    } u;
+    u.v = *reinterpret_cast<const uint4*>(sm + (b - base));
+#pragma unroll
+    for (int i = 0; i < 16 / EB; ++i) u.e[i] = f(u.e[i]);
+    stg128_cs(g + b, u.v);
+  }
+}
+
+// One segment of exactly L items (already in the ordered key space): load,
+// network, store.  The length is a template constant, so each switch case
+// touches exactly L slots and stays small (the order transform runs once per
+// element in the staging passes instead).
+template <int L, class U, class P, int DAG, class CX>
+__device__ __forceinline__ void sort_segment_len(U* keys, P* pays) {
+  constexpr bool HAS_P = !IsNoPay<P>::value;
+  Elem<U, P> v[L];
+#pragma unroll
+  for (int j = 0; j < L; ++j) {
+    v[j].k = keys[j];
+    if constexpr (HAS_P) v[j].p = pays[j];
+  }
+  Net<DAG, L>::template run<CX>(v);
+#pragma unroll
+  for (int j = 0; j < L; ++j) {
+    keys[j] = v[j].k;
+    if constexpr (HAS_P) pays[j] = v[j].p;
   }
 }
 
 template <class U, class P, int DAG, class CX>
-__device__ __forceinline__ void sort_segment_smem(U* keys, P* pays, int len, const Xform& xf) {
-  using E = Elem<U, P>;
-  constexpr bool HAS_P = !IsNoPay<P>::value;
-  E v[16];
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    if (j < len) {
-      U k = keys[j];
-      if (xf.active) k = to_ord<U>(k, xf);
-      v[j].k = k;
-      if constexpr (HAS_P) {
-        P q = pays[j];
-        if (xf.active) q ^= P(xf.pdesc);
-        v[j].p = q;
-      }
-    }
-  }
+__device__ __forceinline__ void sort_segment_smem(U* keys, P* pays, int len) {
   switch (len) {
-    case 2: Net<DAG, 2>::template run<CX>(v); break;
-    case 3: Net<DAG, 3>::template run<CX>(v); break;
-    case 4: Net<DAG, 4>::template run<CX>(v); break;
-    case 5: Net<DAG, 5>::template run<CX>(v); break;
-    case 6: Net<DAG, 6>::template run<CX>(v); break;
-    case 7: Net<DAG, 7>::template run<CX>(v); break;
-    case 8: Net<DAG, 8>::template run<CX>(v); break;
-    case 9: Net<DAG, 9>::template run<CX>(v); break;
-    case 10: Net<DAG, 10>::template run<CX>(v); break;
-    case 11: Net<DAG, 11>::template run<CX>(v); break;
-    case 12: Net<DAG, 12>::template run<CX>(v); break;
-    case 13: Net<DAG, 13>::template run<CX>(v); break;
-    case 14: Net<DAG, 14>::template run<CX>(v); break;
-    case 15: Net<DAG, 15>::template run<CX>(v); break;
-    case 16: Net<DAG, 16>::template run<CX>(v); break;
+    case 2: sort_segment_len<2, U, P, DAG, CX>(keys, pays); break;
+    case 3: sort_segment_len<3, U, P, DAG, CX>(keys, pays); break;
+    case 4: sort_segment_len<4, U, P, DAG, CX>(keys, pays); break;
+    case 5: sort_segment_len<5, U, P, DAG, CX>(keys, pays); break;
+    case 6: sort_segment_len<6, U, P, DAG, CX>(keys, pays); break;
+    case 7: sort_segment_len<7, U, P, DAG, CX>(keys, pays); break;
+    case 8: sort_segment_len<8, U, P, DAG, CX>(keys, pays); break;
+    case 9: sort_segment_len<9, U, P, DAG, CX>(keys, pays); break;
+    case 10: sort_segment_len<10, U, P, DAG, CX>(keys, pays); break;
+    case 11: sort_segment_len<11, U, P, DAG, CX>(keys, pays); break;
+    case 12: sort_segment_len<12, U, P, DAG, CX>(keys, pays); break;
+    case 13: sort_segment_len<13, U, P, DAG, CX>(keys, pays); break;
+    case 14: sort_segment_len<14, U, P, DAG, CX>(keys, pays); break;
+    case 15: sort_segment_len<15, U, P, DAG, CX>(keys, pays); break;
+    case 16: sort_segment_len<16, U, P, DAG, CX>(keys, pays); break;
     default: break;
-  }
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    if (j < len) {
-      U k = v[j].k;
-      if (xf.active) k = from_ord<U>(k, xf);
-      keys[j] = k;
-      if constexpr (HAS_P) {
-        P q = v[j].p;
-        if (xf.active) q ^= P(xf.pdesc);
-        pays[j] = q;
-      }
-    }
   }
 }
 
 template <class U, class P, int MODE, int DAG>
-__global__ void __launch_bounds__(kThreads, 2) seg_kernel(const SegParams prm) {
+__global__ void __launch_bounds__(kThreads, 4) seg_kernel(const SegParams prm) {
   using G = SegGeom<U, P>;
   constexpr bool HAS_P = !IsNoPay<P>::value;
   using CX = typename std::conditional<!HAS_P, CxKeys,
@@ -211,8 +214,16 @@ __global__ void __launch_bounds__(kThreads, 2) seg_kernel(const SegParams prm) {
     const uint32_t e0 = offs[a], e1 = offs[b];
     unsigned char* kb = buf + range_shift<int(sizeof(U))>(e0);
     unsigned char* pb = buf + G::K_REG + (HAS_P ? range_shift<G::PB>(e0) : 0);
-    if (tid < 32) hist[tid] = 0;
-    __syncthreads();
+    // hist[] is zero here (prologue / previous call); callers synchronise first
+    if (staged && xf.active) {  // into the ordered key space, once per element
+      U* kk = reinterpret_cast<U*>(kb);
+      P* pp = reinterpret_cast<P*>(pb);
+      const int ne = int(e1 - e0);
+      for (int i = tid; i < ne; i += kThreads) {
+        kk[i] = to_ord<U>(kk[i], xf);
+        if constexpr (HAS_P) pp[i] ^= P(xf.pdesc);
+      }
+    }
     for (int s = a + tid; s < b; s += kThreads) {
       const int len = int(offs[s + 1] - offs[s]);
       if (len > 16) {
@@ -226,15 +237,16 @@ __global__ void __launch_bounds__(kThreads, 2) seg_kernel(const SegParams prm) {
       }
     }
     __syncthreads();
-    if (tid < 32) {  // exclusive scan over the length bins
-      const int v = hist[tid];
+    if (tid < 32) {  // exclusive scan over the length bins, LONGEST first
+      const int len = 16 - tid;
+      const int v = len >= 2 ? hist[len] : 0;
       int incl = v;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
         const int t = __shfl_up_sync(0xffffffffu, incl, d);
         if (tid >= d) incl += t;
       }
-      cur[tid] = incl - v;
+      if (len >= 2) cur[len] = incl - v;
       if (tid == 31) hist[31] = incl;
     }
     __syncthreads();
@@ -245,21 +257,40 @@ __global__ void __launch_bounds__(kThreads, 2) seg_kernel(const SegParams prm) {
     }
     __syncthreads();
     if (staged) {
-      for (int j = tid; j < nshort; j += kThreads) {
-        const int s = a + perm[j];
-        const int st = int(offs[s] - e0);
-        sort_segment_smem<U, P, DAG, CX>(reinterpret_cast<U*>(kb) + st, reinterpret_cast<P*>(pb) + st,
-                                         int(offs[s + 1] - offs[s]), xf);
+      // warps pull 32-segment chunks, most expensive (longest) first, so the
+      // barrier after this loop waits for balanced work (LPT scheduling)
+      const int lane = tid & 31;
+      for (;;) {
+        int c = 0;
+        if (lane == 0) c = atomicAdd(&hist[30], 1);
+        c = __shfl_sync(0xffffffffu, c, 0);
+        if (c * 32 >= nshort) break;
+        const int j = c * 32 + lane;
+        if (j < nshort) {
+          const int s = a + perm[j];
+          const int st = int(offs[s] - e0);
+          sort_segment_smem<U, P, DAG, CX>(reinterpret_cast<U*>(kb) + st, reinterpret_cast<P*>(pb) + st,
+                                           int(offs[s + 1] - offs[s]));
+        }
       }
-      __syncthreads();
-      store_range<U>(buf, kout, e0, e1, tid);
-      if constexpr (HAS_P) store_range<P>(buf + G::K_REG, pout, e0, e1, tid);
     }
     __syncthreads();
+    if (tid < 32) hist[tid] = 0;  // ready for the next call (after its leading sync)
+    if (staged) {
+      if (xf.active) {
+        store_range<U>(buf, kout, e0, e1, tid, [&](U k) { return from_ord<U>(k, xf); });
+        if constexpr (HAS_P) store_range<P>(buf + G::K_REG, pout, e0, e1, tid, [&](P q) { return P(q ^ P(xf.pdesc)); });
+      } else {
+        store_range<U>(buf, kout, e0, e1, tid, [](U k) { return k; });
+        if constexpr (HAS_P) store_range<P>(buf + G::K_REG, pout, e0, e1, tid, [](P q) { return q; });
+      }
+    }
+    // no trailing barrier: the next tile starts with wait + __syncthreads
   };
 
   int64_t t = blockIdx.x;
   if (t >= ntiles) return;
+  if (tid < 32) hist[tid] = 0;
   // prologue: offsets of tile 0 (synchronously), data of tile 0 + offsets of tile 1 (async)
   issue_offs(t, offs_slot(0));
   cp_async_commit();
@@ -306,12 +337,13 @@ __global__ void __launch_bounds__(kThreads, 2) seg_kernel(const SegParams prm) {
           b = lo;
         }
         staged = offs[b] - offs[a] <= uint32_t(G::CAP);
+        __syncthreads();  // previous sub-tile's stores have read `buf`
         if (staged) {
           issue_data(buf, offs[a], offs[b]);
           cp_async_commit();
           cp_async_wait<0>();
-          __syncthreads();
         }
+        __syncthreads();
       }
       process(offs, a, b, t * TS_, buf, staged);
       a = b;

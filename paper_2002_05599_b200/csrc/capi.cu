@@ -102,6 +102,14 @@ static int launch_geom(const void* fn, int threads, int smem, LaunchGeom* out) {
   return 0;
 }
 
+int kernel_residency(const void* fn, int threads, int smem, int* ctas_per_sm, int* sms) {
+  LaunchGeom g;
+  if (int rc = launch_geom(fn, threads, smem, &g)) return rc;
+  *ctas_per_sm = g.ctas_per_sm;
+  *sms = g.sms;
+  return 0;
+}
+
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 static int launch_net(const KernelInfo& k, NetParams prm, cudaStream_t stream) {

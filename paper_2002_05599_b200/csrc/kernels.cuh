@@ -12,6 +12,9 @@ namespace nsg {
 
 int fail(int code, const char* fmt, ...);
 Xform make_xform(const nsg_spec& sp);
+// cached per (device, kernel): sets the dynamic-smem attribute once and
+// returns resident CTAs per SM and the SM count
+int kernel_residency(const void* fn, int threads, int smem, int* ctas_per_sm, int* sms);
 
 // misc.cu
 int launch_swap_pairs(void* pairs, int64_t m, cudaStream_t st);

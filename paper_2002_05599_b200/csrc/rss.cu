@@ -507,12 +507,8 @@ int launch_rss(const nsg_spec& sp, const void* k_in, void* k_out, const void* p_
   prm.seg_count = seg_count;
   prm.seg_overflow = seg_overflow;
   const RssKernel k = rss_pick(int(n), sp.family == 0 ? 0 : 1, key_bytes, pay, mode, layout);
-  int dev = 0, sms = 0, occ = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (k.smem > 48 * 1024) cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, k.smem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k.fn, k.threads, k.smem);
-  if (occ < 1) return fail(NSG_ERR_CUDA, "RSS kernel cannot be resident (smem %d)", k.smem);
+  int sms = 0, occ = 0;
+  if (int rc = kernel_residency(k.fn, k.threads, k.smem, &occ, &sms)) return rc;
   const int64_t need = (rows + k.warps - 1) / k.warps;
   const int64_t grid = need < int64_t(sms) * occ ? need : int64_t(sms) * occ;
   void* args[] = {&prm};

@@ -30,11 +30,13 @@ namespace nsg {
 
 namespace {
 
-// 128-thread CTAs with ~45 KB of shared memory: 4-5 CTAs per SM, so one
-// CTA's barrier waits are covered by the others
-constexpr int kMaxTileSegs = 256;
-constexpr int kThreads = 128;
-constexpr int kBufBytes = 20 * 1024;  // one staging buffer (keys + payload regions)
+// Large tiles (1024 segments, 8 warps): every length bin of the tile holds
+// enough segments that the 32-segment chunks are (nearly) single-length and
+// the per-tile sort work splits evenly over the warps.  Two staging buffers
+// of 48 KB -> 2 CTAs per SM.
+constexpr int kMaxTileSegs = 1024;
+constexpr int kThreads = 256;
+constexpr int kBufBytes = 48 * 1024;  // one staging buffer (keys + payload regions)
 
 struct SegParams {
   const uint32_t* offsets;
@@ -57,7 +59,7 @@ struct SegGeom {
   static constexpr int CAP = (kBufBytes - 64) / EB / 16 * 16;  // elements per staged (sub)tile
   // segments per tile: ~CAP/7 keeps the expected element count (mean length
   // ~5 for the cfg4 distribution) well inside one staging buffer
-  static constexpr int TS = EB <= 8 ? kMaxTileSegs : kMaxTileSegs / 2;
+  static constexpr int TS = EB <= 8 ? kMaxTileSegs : (EB <= 12 ? kMaxTileSegs * 2 / 3 / 32 * 32 : kMaxTileSegs / 2);
   static constexpr int K_REG = (CAP * int(sizeof(U)) + 32 + 15) / 16 * 16;
   static constexpr int P_REG = PB ? (CAP * PB + 32 + 15) / 16 * 16 : 0;
   static constexpr int BUF = K_REG + P_REG;
@@ -152,9 +154,47 @@ __device__ __forceinline__ void sort_segment_len(U* keys, P* pays) {
   }
 }
 
+// 11..16 items through the 16-channel network with +inf sentinels in the
+// unused top channels.  For the best-known family this executes EXACTLY the
+// reference's 11..15-channel tables (they are top-channel restrictions of
+// Green's 16, networks.py:265-274; a sentinel never moves under strict <), so
+// it is DAG-exact even in REF mode; for any family it is exact in UNIQUE /
+// keys-only mode.  One code path for the long lengths keeps the warps of a
+// mixed-length chunk converged and the kernel's instruction footprint small.
+template <class U, class P, int DAG, class CX>
+__device__ __forceinline__ void sort_segment_pad16(U* keys, P* pays, int len) {
+  constexpr bool HAS_P = !IsNoPay<P>::value;
+  Elem<U, P> v[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    if (j < 11 || j < len) {
+      v[j].k = keys[j];
+      if constexpr (HAS_P) v[j].p = pays[j];
+    } else {
+      v[j].k = U(~U(0));
+      if constexpr (HAS_P) v[j].p = P(~P(0));
+    }
+  }
+  Net<DAG, 16>::template run<CX>(v);
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    if (j < 11 || j < len) {
+      keys[j] = v[j].k;
+      if constexpr (HAS_P) pays[j] = v[j].p;
+    }
+  }
+}
+
 template <class U, class P, int DAG, class CX>
 __device__ __forceinline__ void sort_segment_smem(U* keys, P* pays, int len) {
-  switch (len) {
+  constexpr bool kPad16 = DAG == 0 || !std::is_same<CX, CxRef>::value;
+  if constexpr (kPad16) {
+    if (len >= 11) {
+      sort_segment_pad16<U, P, DAG, CX>(keys, pays, len);
+      return;
+    }
+  }
+  switch (kPad16 ? (len > 10 ? 0 : len) : len) {
     case 2: sort_segment_len<2, U, P, DAG, CX>(keys, pays); break;
     case 3: sort_segment_len<3, U, P, DAG, CX>(keys, pays); break;
     case 4: sort_segment_len<4, U, P, DAG, CX>(keys, pays); break;
@@ -164,18 +204,24 @@ __device__ __forceinline__ void sort_segment_smem(U* keys, P* pays, int len) {
     case 8: sort_segment_len<8, U, P, DAG, CX>(keys, pays); break;
     case 9: sort_segment_len<9, U, P, DAG, CX>(keys, pays); break;
     case 10: sort_segment_len<10, U, P, DAG, CX>(keys, pays); break;
-    case 11: sort_segment_len<11, U, P, DAG, CX>(keys, pays); break;
-    case 12: sort_segment_len<12, U, P, DAG, CX>(keys, pays); break;
-    case 13: sort_segment_len<13, U, P, DAG, CX>(keys, pays); break;
-    case 14: sort_segment_len<14, U, P, DAG, CX>(keys, pays); break;
-    case 15: sort_segment_len<15, U, P, DAG, CX>(keys, pays); break;
-    case 16: sort_segment_len<16, U, P, DAG, CX>(keys, pays); break;
-    default: break;
+    default:
+      if constexpr (!kPad16) {
+        switch (len) {
+          case 11: sort_segment_len<11, U, P, DAG, CX>(keys, pays); break;
+          case 12: sort_segment_len<12, U, P, DAG, CX>(keys, pays); break;
+          case 13: sort_segment_len<13, U, P, DAG, CX>(keys, pays); break;
+          case 14: sort_segment_len<14, U, P, DAG, CX>(keys, pays); break;
+          case 15: sort_segment_len<15, U, P, DAG, CX>(keys, pays); break;
+          case 16: sort_segment_len<16, U, P, DAG, CX>(keys, pays); break;
+          default: break;
+        }
+      }
+      break;
   }
 }
 
 template <class U, class P, int MODE, int DAG>
-__global__ void __launch_bounds__(kThreads, 4) seg_kernel(const SegParams prm) {
+__global__ void __launch_bounds__(kThreads, 2) seg_kernel(const SegParams prm) {
   using G = SegGeom<U, P>;
   constexpr bool HAS_P = !IsNoPay<P>::value;
   using CX = typename std::conditional<!HAS_P, CxKeys,
@@ -398,12 +444,8 @@ int launch_segments(const nsg_spec& sp, const uint32_t* offsets, int64_t nseg, c
   const SegKernel k = dag ? seg_pick_dag<1>(kb, sp.payload_dtype, sp.tie_mode)
                           : seg_pick_dag<0>(kb, sp.payload_dtype, sp.tie_mode);
   SegParams prm{offsets, nseg, keys_in, keys_out, pay_in, pay_out, make_xform(sp), w, w + 4, cap, w + 1};
-  int dev = 0, sms = 0, occ = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, k.smem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k.fn, kThreads, k.smem);
-  if (occ < 1) return fail(NSG_ERR_CUDA, "segment kernel cannot be resident");
+  int sms = 0, occ = 0;
+  if (int rc = kernel_residency(k.fn, kThreads, k.smem, &occ, &sms)) return rc;
   const int64_t ntiles = (nseg + k.ts - 1) / k.ts;
   const int64_t grid = ntiles < int64_t(sms) * occ ? ntiles : int64_t(sms) * occ;
   void* args[] = {&prm};

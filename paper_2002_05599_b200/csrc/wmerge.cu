@@ -183,11 +183,8 @@ int launch_wmerge(const nsg_spec& sp, const void* k_in, void* k_out, const void*
   const int kb = (sp.key_dtype == NSG_KEY_U32 || sp.key_dtype == NSG_KEY_I32 || sp.key_dtype == NSG_KEY_F32) ? 4 : 8;
   const void* fn = wm_pick(kb, sp.payload_dtype, e);
   WmParams prm{k_in, k_out, p_in, p_out, rows, int(n), make_xform(sp)};
-  int dev = 0, sms = 0, occ = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 128, 0);
-  if (occ < 1) return fail(NSG_ERR_CUDA, "warp merge kernel cannot be resident");
+  int sms = 0, occ = 0;
+  if (int rc = kernel_residency(fn, 128, 0, &occ, &sms)) return rc;
   const int64_t need = (rows + 3) / 4;
   const int64_t grid = need < int64_t(sms) * occ ? need : int64_t(sms) * occ;
   void* args[] = {&prm};

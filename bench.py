@@ -74,6 +74,12 @@ class Cell:
     def bytes(self) -> int:  # algorithmic: one read + one write of keys and payloads
         return 2 * self.rows * self.n * (self.kb + self.pb)
 
+    @property
+    def kernel_key(self) -> str:  # name used by tools/profile_summary.py / profiles/traffic.json
+        fam = "best" if self.family == "best" else "bn"
+        pay = {0: "keys", 4: "p32", 8: "p64"}[self.pb]
+        return f"net_sort n={self.n} {fam} {'u64' if self.kb == 8 else 'u32'} {pay} SoA UNIQUE"
+
 
 def make_cells(args, rows):
     ns = [int(x) for x in args.ns.split(",")] if args.ns else list(range(2, 17))
@@ -387,8 +393,9 @@ def main():
             "hbm_gbs_aggregate": round(agg_gbs, 1),
             "hbm_frac_aggregate": round(agg_gbs / peak, 4),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": traffic_for(dom.name),
-                         "kernel": f"net_sort_kernel {dom.name}", "peak_source": peak_src,
+                         "frac": round(achieved / peak, 4), "traffic": traffic_for(dom.kernel_key),
+                         "traffic_source": "profiles/traffic.json (ncu --set full dram__bytes_read+write per launch)",
+                         "kernel": dom.kernel_key, "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": dom.bytes, "avg_launch_ms": round(dom_ms, 4)},
             "per_kernel_gbs": per_kernel,
             "e2e": e2e, "cpu_baseline": cpu,

@@ -62,8 +62,6 @@ KernelInfo net_lookup(int n, int dag, int key_bytes, int pay, int mode, int layo
     case 14: return net_lookup_n14(dag, key_bytes, pay, mode, layout);
     case 15: return net_lookup_n15(dag, key_bytes, pay, mode, layout);
     case 16: return net_lookup_n16(dag, key_bytes, pay, mode, layout);
-    case 32: return net_lookup_n32(dag, key_bytes, pay, mode, layout);
-    case 64: return net_lookup_n64(dag, key_bytes, pay, mode, layout);
     default: return KernelInfo{};
   }
 }
@@ -200,11 +198,13 @@ int nsg_sort_rows(const nsg_spec* sp, const void* keys_in, void* keys_out, const
     }
     if (sp->payload_dtype != NSG_PAY_NONE && sp->tie_mode != NSG_TIE_UNIQUE)
       return fail(NSG_ERR_SPEC, "the merge sorter orders payloads lexicographically: use tie_mode UNIQUE");
-    if (n == 32 || n == 64) {  // thread-per-array odd-even merge network
-      NetParams prm{keys_in, keys_out, pay_in, pay_out, rows, make_xform(*sp)};
-      return launch_net(net_lookup(int(n), 2, kb, sp->payload_dtype, NSG_TIE_UNIQUE, LAYOUT_SOA), prm, st);
+    int g = 0;
+    const KernelInfo mk = merge_lookup(int(n), kb, sp->payload_dtype, &g);
+    if (mk.fn) {  // G lanes per row: sub-row networks + cross-lane bitonic merge
+      NetParams prm{keys_in, keys_out, pay_in, pay_out, rows * g, make_xform(*sp)};
+      return launch_net(mk, prm, st);
     }
-    return launch_wmerge(*sp, keys_in, keys_out, pay_in, pay_out, rows, n, st);
+    return launch_wmerge(*sp, keys_in, keys_out, pay_in, pay_out, rows, n, st);  // any other n: padded
   }
   return fail(NSG_ERR_SPEC, "sorter kind %d is not a batched small-set sorter (out of scope)", sp->kind);
 }

@@ -31,9 +31,11 @@ NSG_DECLARE_NET_LOOKUP(13)
 NSG_DECLARE_NET_LOOKUP(14)
 NSG_DECLARE_NET_LOOKUP(15)
 NSG_DECLARE_NET_LOOKUP(16)
-NSG_DECLARE_NET_LOOKUP(32)
-NSG_DECLARE_NET_LOOKUP(64)
 #undef NSG_DECLARE_NET_LOOKUP
+
+// merge sorter: rows of n items on `*lanes_per_row` lanes (fn == nullptr if
+// n is not G*E for a supported G); launch with rows * lanes_per_row sub-rows
+KernelInfo merge_lookup(int n, int key_bytes, int pay, int* lanes_per_row);
 
 KernelInfo net_lookup(int n, int dag, int key_bytes, int pay, int mode, int layout);
 

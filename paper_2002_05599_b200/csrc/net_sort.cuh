@@ -132,10 +132,16 @@ __device__ __forceinline__ void word_put(uint32_t* w, int j, uint64_t v) {
   w[2 * j + 1] = uint32_t(v >> 32);
 }
 
-// Compile-time configuration of one kernel instance.
-template <int N_, int DAG_, class U_, class P_, int MODE_, int LAYOUT_>
+// Compile-time configuration of one kernel instance.  G > 1 (merge sorter):
+// a row of G*N items is split into G contiguous sub-rows of N, one per lane;
+// each lane sorts its sub-row with Net<DAG, N>, then the G lanes merge with
+// bitonic flip/half-cleaner stages over __shfl_xor_sync (merge_lanes below).
+// All tile staging works on sub-rows, so it is unchanged.
+template <int N_, int DAG_, class U_, class P_, int MODE_, int LAYOUT_, int G_ = 1>
 struct NetCfg {
   static constexpr int N = N_;
+  static constexpr int G = G_;
+  static_assert(G >= 1 && G <= 32 && (G & (G - 1)) == 0, "G: power of two <= 32");
   static constexpr int DAG = DAG_;
   using U = U_;
   using P = P_;
@@ -254,6 +260,86 @@ __device__ __forceinline__ void load_row_elems(const unsigned char* smk, const u
   }
 }
 
+template <class T>
+__device__ __forceinline__ T shfl_xor_any(T v, int m) {
+  if constexpr (sizeof(T) == 8) {
+    const uint32_t lo = __shfl_xor_sync(0xffffffffu, uint32_t(uint64_t(v)), m);
+    const uint32_t hi = __shfl_xor_sync(0xffffffffu, uint32_t(uint64_t(v) >> 32), m);
+    return T(uint64_t(lo) | (uint64_t(hi) << 32));
+  } else {
+    return T(__shfl_xor_sync(0xffffffffu, uint32_t(v), m));
+  }
+}
+
+// keep the partner's element o instead of a iff it is the min (keep_min) / max
+template <class Cfg>
+__device__ __forceinline__ void keep(Elem<typename Cfg::U, typename Cfg::P>& a,
+                                     const Elem<typename Cfg::U, typename Cfg::P>& o, bool keep_min) {
+  bool olt, alt;
+  if constexpr (Cfg::HAS_P) {
+    olt = lex_lt(o.k, o.p, a.k, a.p);
+    alt = lex_lt(a.k, a.p, o.k, o.p);
+  } else {
+    olt = key_lt(o.k, a.k);
+    alt = key_lt(a.k, o.k);
+  }
+  const bool take = keep_min ? olt : alt;
+  a.k = take ? o.k : a.k;
+  if constexpr (Cfg::HAS_P) a.p = take ? o.p : a.p;
+}
+
+template <class Cfg>
+__device__ __forceinline__ Elem<typename Cfg::U, typename Cfg::P> shfl_elem(
+    const Elem<typename Cfg::U, typename Cfg::P>& v, int m) {
+  Elem<typename Cfg::U, typename Cfg::P> o;
+  o.k = shfl_xor_any(v.k, m);
+  if constexpr (Cfg::HAS_P) o.p = shfl_xor_any(v.p, m);
+  return o;
+}
+
+// Merge G lanes' sorted sub-rows (lane gl holds positions gl*N .. gl*N+N-1)
+// into one sorted row: for every doubling m, a FLIP stage (partner lane
+// gl ^ (2m-1), register N-1-r: min stays with the lower half), cross-lane
+// half-cleaners (partner gl ^ j), then an in-register bitonic merge of N.
+// All ascending -- no per-lane direction bits.  Every lane of the warp must
+// call this (shuffles use the full mask).
+template <class Cfg>
+__device__ __forceinline__ void merge_lanes(Elem<typename Cfg::U, typename Cfg::P> (&e)[Cfg::N]) {
+  using E = Elem<typename Cfg::U, typename Cfg::P>;
+  constexpr int G = Cfg::G, N = Cfg::N;
+  const int gl = int(threadIdx.x) & (G - 1);
+#pragma unroll
+  for (int m = 1; m < G; m <<= 1) {
+    const bool flip_min = (gl & m) == 0;
+#pragma unroll
+    for (int r = 0; r < N / 2; ++r) {
+      const E o1 = shfl_elem<Cfg>(e[N - 1 - r], 2 * m - 1);  // partner of e[r]
+      const E o2 = shfl_elem<Cfg>(e[r], 2 * m - 1);          // partner of e[N-1-r]
+      keep<Cfg>(e[r], o1, flip_min);
+      keep<Cfg>(e[N - 1 - r], o2, flip_min);
+    }
+    if constexpr (N == 1) {
+      const E o = shfl_elem<Cfg>(e[0], 2 * m - 1);
+      keep<Cfg>(e[0], o, flip_min);
+    }
+#pragma unroll
+    for (int j = m >> 1; j >= 1; j >>= 1) {
+      const bool km = (gl & j) == 0;
+#pragma unroll
+      for (int r = 0; r < N; ++r) {
+        const E o = shfl_elem<Cfg>(e[r], j);
+        keep<Cfg>(e[r], o, km);
+      }
+    }
+#pragma unroll
+    for (int j = N / 2; j >= 1; j >>= 1) {
+#pragma unroll
+      for (int r = 0; r < N; ++r)
+        if ((r & j) == 0) Cfg::CX::cx(e[r], e[r | j]);
+    }
+  }
+}
+
 template <class Cfg>
 __device__ __forceinline__ void sort_elems(Elem<typename Cfg::U, typename Cfg::P> (&e)[Cfg::N], const Xform& xf) {
   using U = typename Cfg::U;
@@ -267,6 +353,7 @@ __device__ __forceinline__ void sort_elems(Elem<typename Cfg::U, typename Cfg::P
     }
   }
   Net<Cfg::DAG, N>::template run<typename Cfg::CX>(e);
+  if constexpr (Cfg::G > 1) merge_lanes<Cfg>(e);
   if (xf.active) {
 #pragma unroll
     for (int j = 0; j < N; ++j) {
@@ -405,9 +492,9 @@ __global__ void __launch_bounds__(Cfg::WARPS * 32) net_sort_kernel(const NetPara
     unsigned char* smp = smk + Cfg::K_SMEM;
     const int64_t row0 = t * ROWS;
     const int vrows = p.rows - row0 < ROWS ? int(p.rows - row0) : ROWS;
-    if constexpr (Cfg::APL == 1) {
+    if constexpr (Cfg::APL == 1 && Cfg::G == 1) {
       if (lane < vrows) sort_row<Cfg>(smk, smp, lane, p.xf);
-    } else {
+    } else {  // (G > 1: every lane runs the merge shuffles; only valid rows load/store)
       Elem<typename Cfg::U, typename Cfg::P> e[Cfg::APL][Cfg::N];
 #pragma unroll
       for (int a = 0; a < Cfg::APL; ++a)

@@ -1,18 +1,20 @@
-// One translation unit per row length N (compiled with -DNSG_N=<N>): all
-// (DAG, key width, payload, tie mode, layout) instances of net_sort_kernel.
+// Instantiation units of net_sort_kernel, compiled in parallel:
+//   -DNSG_N=<1..16>  all (DAG, key width, payload, tie mode, layout) instances
+//                    for rows of N items (one thread per row);
+//   -DNSG_N=0        the merge sorter: rows of G*E items, G lanes per row.
 #include "dispatch.h"
 #include "net_sort.cuh"
 
 #ifndef NSG_N
-#error "compile with -DNSG_N=<row length>"
+#error "compile with -DNSG_N=<row length> (0 = merge sorter unit)"
 #endif
 
 namespace nsg {
 namespace {
 
-template <int N, int DAG, class U, class P, int MODE, int LAYOUT>
+template <int N, int DAG, class U, class P, int MODE, int LAYOUT, int G = 1>
 KernelInfo info() {
-  using C = NetCfg<N, DAG, U, P, MODE, LAYOUT>;
+  using C = NetCfg<N, DAG, U, P, MODE, LAYOUT, G>;
   KernelInfo k;
   k.fn = reinterpret_cast<const void*>(&net_sort_kernel<C>);
   k.smem = C::CTA_SMEM;
@@ -22,6 +24,20 @@ KernelInfo info() {
   return k;
 }
 
+#if NSG_N == 0
+template <class U, class P, int E, int DAGM>
+KernelInfo merge_g(int g) {
+  switch (g) {
+    case 1: return info<E, DAGM, U, P, MODE_UNIQUE, LAYOUT_SOA, 1>();
+    case 2: return info<E, DAGM, U, P, MODE_UNIQUE, LAYOUT_SOA, 2>();
+    case 4: return info<E, DAGM, U, P, MODE_UNIQUE, LAYOUT_SOA, 4>();
+    case 8: return info<E, DAGM, U, P, MODE_UNIQUE, LAYOUT_SOA, 8>();
+    case 16: return info<E, DAGM, U, P, MODE_UNIQUE, LAYOUT_SOA, 16>();
+    case 32: return info<E, DAGM, U, P, MODE_UNIQUE, LAYOUT_SOA, 32>();
+    default: return KernelInfo{};
+  }
+}
+#else
 template <int N, int DAG>
 KernelInfo lookup_dag(int key_bytes, int pay, int mode, int layout) {
   if (layout == LAYOUT_AOS16)
@@ -42,25 +58,32 @@ KernelInfo lookup_dag(int key_bytes, int pay, int mode, int layout) {
   return mode ? info<N, DAG, uint64_t, uint64_t, MODE_UNIQUE, LAYOUT_SOA>()
               : info<N, DAG, uint64_t, uint64_t, MODE_REF, LAYOUT_SOA>();
 }
+#endif
 
 }  // namespace
 
-#define NSG_CAT2(a, b) a##b
-#define NSG_CAT(a, b) NSG_CAT2(a, b)
-#if NSG_N > 16
-// 32 / 64 items: the odd-even merge network (DAG 2), keys-only or UNIQUE payload
-KernelInfo NSG_CAT(net_lookup_n, NSG_N)(int dag, int key_bytes, int pay, int mode, int layout) {
-  if (dag != 2 || layout != LAYOUT_SOA || (pay != 0 && mode != MODE_UNIQUE)) return KernelInfo{};
+#if NSG_N == 0
+// Merge sorter (kind MERGE), keys-only or UNIQUE (key, payload):
+//  keys-only: E = 32 per lane (odd-even merge network, DAG 2), n = 32..1024;
+//  with payload: E = 16 per lane (Green-16), n = 32..512.
+KernelInfo merge_lookup(int n, int key_bytes, int pay, int* lanes_per_row) {
+  const int e = pay == 0 ? 32 : 16;
+  if (n % e) return KernelInfo{};
+  const int g = n / e;
+  if (g < 1 || g > 32 || (g & (g - 1)) || (pay != 0 && g < 2)) return KernelInfo{};
+  *lanes_per_row = g;
   if (key_bytes == 4) {
-    if (pay == 0) return info<NSG_N, 2, uint32_t, NoPay, MODE_UNIQUE, LAYOUT_SOA>();
-    if (pay == 1) return info<NSG_N, 2, uint32_t, uint32_t, MODE_UNIQUE, LAYOUT_SOA>();
-    return info<NSG_N, 2, uint32_t, uint64_t, MODE_UNIQUE, LAYOUT_SOA>();
+    if (pay == 0) return merge_g<uint32_t, NoPay, 32, 2>(g);
+    if (pay == 1) return merge_g<uint32_t, uint32_t, 16, 0>(g);
+    return merge_g<uint32_t, uint64_t, 16, 0>(g);
   }
-  if (pay == 0) return info<NSG_N, 2, uint64_t, NoPay, MODE_UNIQUE, LAYOUT_SOA>();
-  if (pay == 1) return info<NSG_N, 2, uint64_t, uint32_t, MODE_UNIQUE, LAYOUT_SOA>();
-  return info<NSG_N, 2, uint64_t, uint64_t, MODE_UNIQUE, LAYOUT_SOA>();
+  if (pay == 0) return merge_g<uint64_t, NoPay, 32, 2>(g);
+  if (pay == 1) return merge_g<uint64_t, uint32_t, 16, 0>(g);
+  return merge_g<uint64_t, uint64_t, 16, 0>(g);
 }
 #else
+#define NSG_CAT2(a, b) a##b
+#define NSG_CAT(a, b) NSG_CAT2(a, b)
 KernelInfo NSG_CAT(net_lookup_n, NSG_N)(int dag, int key_bytes, int pay, int mode, int layout) {
   return dag ? lookup_dag<NSG_N, 1>(key_bytes, pay, mode, layout)
              : lookup_dag<NSG_N, 0>(key_bytes, pay, mode, layout);

@@ -131,7 +131,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            self._stop.wait(0.05)
+            self._stop.wait(0.01)
 
     def __enter__(self):
         if self.nv:
@@ -430,9 +430,27 @@ def verify(cells, inputs, out_k, out_p, launch, dev):
             pay_in = pbuf[: m * c.n * c.pb].cpu().numpy().view(pd).reshape(m, c.n)
             got_p = out_p[: m * c.n * c.pb].cpu().numpy().view(pd).reshape(m, c.n)
         ek, ep = oracle.typed_sort_rows(keys_in, pay_in, family=c.family, unique=c.unique)
+        from paper_2002_05599_b200.errors import CorrectnessFailure
         if not np.array_equal(ek, got_k) or (c.pb and not np.array_equal(ep, got_p)):
-            from paper_2002_05599_b200.errors import CorrectnessFailure
-            raise CorrectnessFailure(f"bench verification failed for {c.name}")
+            raise CorrectnessFailure(f"bench verification failed for {c.name} (oracle prefix)")
+        # every row of the launch: ordered + permutation of its input, on device
+        bad = verify_device(c, kbuf, pbuf, out_k, out_p, dev)
+        if bad:
+            raise CorrectnessFailure(f"bench verification failed for {c.name}: {bad} bad rows (device check)")
+
+
+def verify_device(c, kbuf, pbuf, out_k, out_p, dev) -> int:
+    import torch
+
+    from paper_2002_05599_b200 import _lib, registry
+    order = registry.DeviceOrder(registry.KEY_DTYPES[c.key_dtype], registry.PAY_DTYPES[c.pay_dtype], 0,
+                                 registry.TIE_UNIQUE if c.unique else registry.TIE_REF)
+    sp = _lib.make_spec(registry.spec_network(c.family, "4CmS"), order)
+    bad = torch.zeros(1, dtype=torch.int64, device=dev)
+    _lib.check(_lib.lib().nsg_verify_rows(sp, kbuf.data_ptr(), pbuf.data_ptr() if pbuf is not None else None,
+                                          out_k.data_ptr(), out_p.data_ptr() if pbuf is not None else None,
+                                          c.rows, c.n, bad.data_ptr(), _lib.current_stream_handle(dev)))
+    return int(bad.item())
 
 
 def run_e2e(cells, batch, dev, world, rank, steps):

@@ -96,6 +96,17 @@ size_t nsg_segments_ws_bytes(int64_t nseg, int64_t nelem);
 int nsg_sort_segments(const nsg_spec* sp, const uint32_t* offsets, int64_t nseg, const void* keys_in,
                       void* keys_out, const void* pay_in, void* pay_out, void* ws, size_t ws_bytes, void* stream);
 
+/* On-device verification (the reference's sorted scan + multiset check,
+ * netsort_core.c:56-100,642-657): counts into *bad_rows (DEVICE memory) the
+ * rows / segments whose output is not ordered under the spec or is not a
+ * permutation of the input (order-independent 64-bit hashes of the
+ * (key, payload) pairs).  Stream-ordered; read *bad after synchronising. */
+int nsg_verify_rows(const nsg_spec* sp, const void* keys_in, const void* pay_in, const void* keys_out,
+                    const void* pay_out, int64_t rows, int64_t n, unsigned long long* bad_rows, void* stream);
+int nsg_verify_segments(const nsg_spec* sp, const uint32_t* offsets, int64_t nseg, const void* keys_in,
+                        const void* pay_in, const void* keys_out, const void* pay_out,
+                        unsigned long long* bad_segments, void* stream);
+
 /* Replaces `_native.swap_pairs(code, rows)` / `ns_cswap_dyn` (netsort_core.c:106-118):
  * one conditional swap per (left, right) pair of DEVICE items. */
 int nsg_swap_pairs(int code, void* pairs, int64_t m, void* stream);

@@ -29,6 +29,7 @@ EXPORTS = (
     "nsg_run_sorter_many", "nsg_run_sorter_many_host", "nsg_sort_rows", "nsg_sort_rows_host",
     "nsg_segments_ws_bytes", "nsg_sort_segments", "nsg_swap_pairs", "nsg_classify_block",
     "nsg_lcg_next", "nsg_fill_splitmix", "nsg_last_error", "nsg_version",
+    "nsg_verify_rows", "nsg_verify_segments",
 )
 
 
@@ -74,6 +75,8 @@ _SIGS = {
                                           ctypes.c_uint64, ctypes.c_int, _P, _P]),
     "nsg_lcg_next": (ctypes.c_uint32, [ctypes.c_uint32]),
     "nsg_fill_splitmix": (ctypes.c_int, [_P, _I64, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, _P]),
+    "nsg_verify_rows": (ctypes.c_int, [ctypes.POINTER(NsgSpec), _P, _P, _P, _P, _I64, _I64, _P, _P]),
+    "nsg_verify_segments": (ctypes.c_int, [ctypes.POINTER(NsgSpec), _P, _I64, _P, _P, _P, _P, _P, _P]),
     "nsg_last_error": (ctypes.c_char_p, []),
     "nsg_version": (ctypes.c_int, []),
 }

@@ -109,6 +109,33 @@ def sort_rows(keys, payload=None, *, kind: str = "network", family: str = "best"
     return ok, op
 
 
+def verify_rows(keys_in, keys_out, payload_in=None, payload_out=None, *, descending: bool = False,
+                tie: str = "unique") -> int:
+    """On-device check of a sort_rows result (CUDA tensors): number of rows that
+    are not ordered or not a permutation of their input (0 = all good)."""
+    import torch
+    rows, n = int(keys_in.shape[0]), int(keys_in.shape[1])
+    sp = make_spec(registry.spec_network("best", "4CmS"), make_order(keys_in, payload_in, descending, tie))
+    bad = torch.zeros(1, dtype=torch.int64, device=keys_in.device)
+    check(lib().nsg_verify_rows(sp, keys_in.data_ptr(), payload_in.data_ptr() if payload_in is not None else None,
+                                keys_out.data_ptr(), payload_out.data_ptr() if payload_out is not None else None,
+                                rows, n, bad.data_ptr(), current_stream_handle(keys_in.device)))
+    return int(bad.item())
+
+
+def verify_segments(offsets, keys_in, keys_out, payload_in=None, payload_out=None, *, descending: bool = False,
+                    tie: str = "unique") -> int:
+    """On-device check of a sort_segments result (CUDA tensors): bad segment count."""
+    import torch
+    sp = make_spec(registry.spec_network("best", "4CmS"), make_order(keys_in, payload_in, descending, tie))
+    bad = torch.zeros(1, dtype=torch.int64, device=keys_in.device)
+    check(lib().nsg_verify_segments(sp, offsets.data_ptr(), int(offsets.numel()) - 1, keys_in.data_ptr(),
+                                    payload_in.data_ptr() if payload_in is not None else None, keys_out.data_ptr(),
+                                    payload_out.data_ptr() if payload_out is not None else None, bad.data_ptr(),
+                                    current_stream_handle(keys_in.device)))
+    return int(bad.item())
+
+
 def sort_segments(offsets, keys, payload=None, *, family: str = "best", swap: str = "4CmS",
                   descending: bool = False, tie: str = "unique", out_keys=None, out_payload=None,
                   workspace=None):

@@ -354,6 +354,27 @@ int nsg_fill_splitmix(void* out, int64_t count, int elem_bytes, uint64_t seed, u
 
 size_t nsg_segments_ws_bytes(int64_t nseg, int64_t nelem) { return segments_ws_bytes(nseg, nelem); }
 
+int nsg_verify_rows(const nsg_spec* sp, const void* keys_in, const void* pay_in, const void* keys_out,
+                    const void* pay_out, int64_t rows, int64_t n, unsigned long long* bad_rows, void* stream) {
+  g_err.clear();
+  if (int rc = check_common(sp)) return rc;
+  if (!key_bytes_of(sp->key_dtype)) return fail(NSG_ERR_SPEC, "unknown key dtype %d", sp->key_dtype);
+  if (rows <= 0 || n <= 0) return 0;
+  return launch_verify_rows(*sp, keys_in, pay_in, keys_out, pay_out, rows, n, bad_rows,
+                            static_cast<cudaStream_t>(stream));
+}
+
+int nsg_verify_segments(const nsg_spec* sp, const uint32_t* offsets, int64_t nseg, const void* keys_in,
+                        const void* pay_in, const void* keys_out, const void* pay_out, unsigned long long* bad_segments,
+                        void* stream) {
+  g_err.clear();
+  if (int rc = check_common(sp)) return rc;
+  if (!key_bytes_of(sp->key_dtype)) return fail(NSG_ERR_SPEC, "unknown key dtype %d", sp->key_dtype);
+  if (nseg <= 0) return 0;
+  return launch_verify_segments(*sp, offsets, nseg, keys_in, pay_in, keys_out, pay_out, bad_segments,
+                                static_cast<cudaStream_t>(stream));
+}
+
 int nsg_sort_segments(const nsg_spec* sp, const uint32_t* offsets, int64_t nseg, const void* keys_in,
                       void* keys_out, const void* pay_in, void* pay_out, void* ws, size_t ws_bytes, void* stream) {
   g_err.clear();

@@ -35,6 +35,12 @@ int launch_rss_segment_list(const nsg_spec& sp, const uint32_t* offsets, const u
 int launch_wmerge(const nsg_spec& sp, const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows,
                   int64_t n, cudaStream_t st);
 
+// verify.cu
+int launch_verify_rows(const nsg_spec& sp, const void* ki, const void* pi, const void* ko, const void* po,
+                       int64_t rows, int64_t n, unsigned long long* bad, cudaStream_t st);
+int launch_verify_segments(const nsg_spec& sp, const uint32_t* off, int64_t nseg, const void* ki, const void* pi,
+                           const void* ko, const void* po, unsigned long long* bad, cudaStream_t st);
+
 // segments.cu
 size_t segments_ws_bytes(int64_t nseg, int64_t nelem);
 int launch_segments(const nsg_spec& sp, const uint32_t* offsets, int64_t nseg, const void* keys_in, void* keys_out,

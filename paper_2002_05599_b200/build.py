@@ -47,18 +47,23 @@ def _stale(target: Path, deps: list) -> bool:
 
 
 def build(force: bool = False, jobs: int | None = None, verbose: bool = False, defines: tuple = (),
-          lib_path: Path | None = None, obj_dir: Path | None = None) -> Path:
+          lib_path: Path | None = None, obj_dir: Path | None = None, only: str | None = None) -> Path:
     """Build libnsg.so.  `defines` / `lib_path` / `obj_dir` build tuning
-    variants (tools/variants.py) next to, never instead of, the product."""
+    variants (tools/variants.py) next to, never instead of, the product;
+    `only` (prefix of object names, e.g. "net_") recompiles just those units
+    with the defines and links the rest from the product's objects."""
     subprocess.run([sys.executable, str(ROOT / "tools" / "gen_networks.py")], check=True,
                    stdout=None if verbose else subprocess.DEVNULL)
-    OBJ = Path(obj_dir) if obj_dir else globals()["OBJ"]
+    main_obj = globals()["OBJ"]
+    OBJ = Path(obj_dir) if obj_dir else main_obj
     LIB = Path(lib_path) if lib_path else globals()["LIB"]
     OBJ.mkdir(parents=True, exist_ok=True)
     headers = _headers()
     todo = []
     for obj, src, extra in _units():
         out = OBJ / obj
+        if only and not obj.startswith(only):
+            continue
         if force or _stale(out, [src] + headers):
             todo.append((out, src, extra))
 
@@ -76,7 +81,7 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False, d
             for out in ex.map(compile_one, todo):
                 if verbose:
                     print("compiled", out.name)
-    objs = [OBJ / o for o, _, _ in _units()]
+    objs = [(OBJ if (not only or o.startswith(only)) else main_obj) / o for o, _, _ in _units()]
     if force or todo or _stale(LIB, objs):
         tmp = LIB.with_suffix(".so.tmp")
         cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", str(tmp)] + [str(o) for o in objs]

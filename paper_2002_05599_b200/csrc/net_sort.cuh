@@ -35,6 +35,9 @@
 #ifndef NSG_WARPS
 #define NSG_WARPS 4
 #endif
+#ifndef NSG_NO_NETWORK
+#define NSG_NO_NETWORK 0
+#endif
 
 namespace nsg {
 
@@ -352,8 +355,10 @@ __device__ __forceinline__ void sort_elems(Elem<typename Cfg::U, typename Cfg::P
       if constexpr (Cfg::HAS_P) e[j].p ^= P(xf.pdesc);
     }
   }
+#if !NSG_NO_NETWORK  // (experiment knob: pipeline cost without the network)
   Net<Cfg::DAG, N>::template run<typename Cfg::CX>(e);
   if constexpr (Cfg::G > 1) merge_lanes<Cfg>(e);
+#endif
   if (xf.active) {
 #pragma unroll
     for (int j = 0; j < N; ++j) {
@@ -420,7 +425,9 @@ __device__ __forceinline__ void sort_row(unsigned char* smk, unsigned char* smp,
       if constexpr (Cfg::HAS_P) e[j].p ^= P(xf.pdesc);
     }
   }
+#if !NSG_NO_NETWORK
   Net<Cfg::DAG, N>::template run<typename Cfg::CX>(e);
+#endif
   if (xf.active) {
 #pragma unroll
     for (int j = 0; j < N; ++j) {
@@ -448,8 +455,53 @@ __device__ __forceinline__ void sort_row(unsigned char* smk, unsigned char* smp,
   }
 }
 
+// Experiment knob NSG_DIRECT_STORE: lanes write their sorted rows straight
+// from registers to HBM (vector stores, 2x L2 write transactions) instead of
+// the shared-memory round trip + coalesced tile store.
+#ifndef NSG_DIRECT_STORE
+#define NSG_DIRECT_STORE 0
+#endif
+template <class G>
+__device__ __forceinline__ void stg_row(unsigned char* g, const uint32_t (&w)[G::W]) {
+#pragma unroll
+  for (int i = 0; i < G::R / G::V; ++i) {
+    if constexpr (G::V == 16) {
+      stg128_cs(g + 16 * i, make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]));
+    } else if constexpr (G::V == 8) {
+      *reinterpret_cast<uint2*>(g + 8 * i) = make_uint2(w[2 * i], w[2 * i + 1]);
+    } else {
+      *reinterpret_cast<uint32_t*>(g + 4 * i) = w[i];
+    }
+  }
+}
 template <class Cfg>
-__global__ void __launch_bounds__(Cfg::WARPS * 32) net_sort_kernel(const NetParams p) {
+__device__ __forceinline__ void store_row_global(unsigned char* kout, unsigned char* pout, int64_t row,
+                                                 const Elem<typename Cfg::U, typename Cfg::P> (&e)[Cfg::N]) {
+  constexpr int N = Cfg::N;
+  uint32_t wk[Cfg::GK::W];
+  if constexpr (Cfg::LAYOUT == LAYOUT_AOS16) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      word_put(wk, 2 * j, e[j].k);
+      word_put(wk, 2 * j + 1, e[j].p);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < N; ++j) word_put(wk, j, e[j].k);
+  }
+  stg_row<typename Cfg::GK>(kout + row * Cfg::GK::R, wk);
+  if constexpr (Cfg::PEB != 0) {
+    uint32_t wp[Cfg::GP::W];
+#pragma unroll
+    for (int j = 0; j < N; ++j) word_put(wp, j, e[j].p);
+    stg_row<typename Cfg::GP>(pout + row * Cfg::GP::R, wp);
+  }
+}
+
+// (min 1 CTA/SM: occupancy is set by shared memory; without it ptxas caps
+// registers low enough to spill the small-N instances)
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::WARPS * 32, 1) net_sort_kernel(const NetParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -492,7 +544,7 @@ __global__ void __launch_bounds__(Cfg::WARPS * 32) net_sort_kernel(const NetPara
     unsigned char* smp = smk + Cfg::K_SMEM;
     const int64_t row0 = t * ROWS;
     const int vrows = p.rows - row0 < ROWS ? int(p.rows - row0) : ROWS;
-    if constexpr (Cfg::APL == 1 && Cfg::G == 1) {
+    if constexpr (Cfg::APL == 1 && Cfg::G == 1 && !NSG_DIRECT_STORE) {
       if (lane < vrows) sort_row<Cfg>(smk, smp, lane, p.xf);
     } else {  // (G > 1: every lane runs the merge shuffles; only valid rows load/store)
       Elem<typename Cfg::U, typename Cfg::P> e[Cfg::APL][Cfg::N];
@@ -501,14 +553,22 @@ __global__ void __launch_bounds__(Cfg::WARPS * 32) net_sort_kernel(const NetPara
         if (a * 32 + lane < vrows) load_row_elems<Cfg>(smk, smp, a * 32 + lane, e[a]);
 #pragma unroll
       for (int a = 0; a < Cfg::APL; ++a) sort_elems<Cfg>(e[a], p.xf);
+#if NSG_DIRECT_STORE
+#pragma unroll
+      for (int a = 0; a < Cfg::APL; ++a)
+        if (a * 32 + lane < vrows) store_row_global<Cfg>(kout, pout, row0 + a * 32 + lane, e[a]);
+#else
 #pragma unroll
       for (int a = 0; a < Cfg::APL; ++a)
         if (a * 32 + lane < vrows) store_row_elems<Cfg>(smk, smp, a * 32 + lane, e[a]);
+#endif
     }
+#if !NSG_DIRECT_STORE
     __syncwarp();
     store_region<typename Cfg::GK, ROWS>(smk, kout + row0 * Cfg::GK::R, vrows * Cfg::GK::R, lane);
     if constexpr (Cfg::PEB != 0)
       store_region<typename Cfg::GP, ROWS>(smp, pout + row0 * Cfg::GP::R, vrows * Cfg::GP::R, lane);
+#endif
     __syncwarp();
     stage = (stage + 1) % S;
   }

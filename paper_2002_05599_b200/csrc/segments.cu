@@ -85,12 +85,14 @@ template <int EB>
 __device__ __forceinline__ void issue_range(unsigned char* dst, const unsigned char* src, uint32_t e0, uint32_t e1,
                                             uint64_t limit_bytes, int tid) {
   const uint64_t c0 = (uint64_t(e0) * EB) >> 4;
-  const uint64_t c1 = (uint64_t(e1) * EB + 15) >> 4;
-  for (uint64_t c = c0 + tid; c < c1; c += kThreads) {
-    const uint64_t g = c << 4;
-    const int64_t rem = int64_t(limit_bytes) - int64_t(g);
+  const int nch = int(((uint64_t(e1) * EB + 15) >> 4) - c0);
+  const unsigned char* gbase = src + (c0 << 4);
+  const int64_t lim = int64_t(limit_bytes) - int64_t(c0 << 4);  // bytes readable from gbase
+  for (int c = tid; c < nch; c += kThreads) {
+    const int off = c << 4;
+    const int64_t rem = lim - off;
     const int nb = rem >= 16 ? 16 : (rem > 0 ? int(rem) : 0);
-    cp_async16(dst + ((c - c0) << 4), nb ? src + g : src, nb);
+    cp_async16(dst + off, nb ? gbase + off : gbase, nb);
   }
 }
 template <int EB>
@@ -261,13 +263,30 @@ __global__ void __launch_bounds__(kThreads, 2) seg_kernel(const SegParams prm) {
     unsigned char* kb = buf + range_shift<int(sizeof(U))>(e0);
     unsigned char* pb = buf + G::K_REG + (HAS_P ? range_shift<G::PB>(e0) : 0);
     // hist[] is zero here (prologue / previous call); callers synchronise first
-    if (staged && xf.active) {  // into the ordered key space, once per element
-      U* kk = reinterpret_cast<U*>(kb);
-      P* pp = reinterpret_cast<P*>(pb);
-      const int ne = int(e1 - e0);
-      for (int i = tid; i < ne; i += kThreads) {
-        kk[i] = to_ord<U>(kk[i], xf);
-        if constexpr (HAS_P) pp[i] ^= P(xf.pdesc);
+    if (staged && xf.active) {  // into the ordered key space, once per element,
+      // 16 bytes at a time over the whole staged chunk range (edge elements of
+      // the neighbouring tiles are transformed too, but never stored)
+      const int kchunks = int((uint64_t(e1) * sizeof(U) + 15) / 16 - (uint64_t(e0) * sizeof(U)) / 16);
+      for (int c = tid; c < kchunks; c += kThreads) {
+        union {
+          uint4 v;
+          U e[16 / sizeof(U)];
+        } u;
+        u.v = reinterpret_cast<uint4*>(buf)[c];
+#pragma unroll
+        for (int i = 0; i < int(16 / sizeof(U)); ++i) u.e[i] = to_ord<U>(u.e[i], xf);
+        reinterpret_cast<uint4*>(buf)[c] = u.v;
+      }
+      if constexpr (HAS_P) {
+        if (xf.pdesc) {
+          const int pchunks = int((uint64_t(e1) * G::PB + 15) / 16 - (uint64_t(e0) * G::PB) / 16);
+          uint4* pc = reinterpret_cast<uint4*>(buf + G::K_REG);
+          for (int c = tid; c < pchunks; c += kThreads) {
+            uint4 x = pc[c];
+            x.x = ~x.x; x.y = ~x.y; x.z = ~x.z; x.w = ~x.w;
+            pc[c] = x;
+          }
+        }
       }
     }
     for (int s = a + tid; s < b; s += kThreads) {

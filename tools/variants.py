@@ -22,11 +22,9 @@ sys.path.insert(0, str(ROOT))
 
 VARIANTS = {
     "base": (),
-    "tile8k": ("NSG_TILE_BYTES=8192",),
-    "st4": ("NSG_STAGES=4",),
-    "plainst": ("NSG_STG_CS=0",),
-    "w8": ("NSG_WARPS=8", "NSG_STAGES=2"),
-    "tile8k_st2": ("NSG_TILE_BYTES=8192", "NSG_STAGES=2"),
+    "nonet": ("NSG_NO_NETWORK=1",),  # pipeline + smem transpose only: the kernel's memory ceiling
+    "dstore": ("NSG_DIRECT_STORE=1",),
+    "dstore_st4": ("NSG_DIRECT_STORE=1", "NSG_STAGES=4"),
 }
 CELLS = [(2, 8, 0), (3, 8, 0), (4, 8, 0), (8, 8, 0), (12, 8, 0), (16, 8, 0), (4, 8, 4), (16, 8, 4), (16, 8, 8),
          (8, 4, 0)]
@@ -36,7 +34,7 @@ def build_all():
     from paper_2002_05599_b200.build import build
     for name, defs in VARIANTS.items():
         d = ROOT / "variants" / name
-        build(defines=defs, lib_path=d / "libnsg.so", obj_dir=d / "obj", jobs=8)
+        build(defines=defs, lib_path=d / "libnsg.so", obj_dir=d / "obj", jobs=8, only="net_n")
         print("built", name, flush=True)
 
 

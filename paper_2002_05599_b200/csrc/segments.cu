@@ -35,7 +35,7 @@ namespace {
 // the per-tile sort work splits evenly over the warps.  Two staging buffers
 // of 48 KB -> 2 CTAs per SM.
 constexpr int kMaxTileSegs = 1024;
-constexpr int kThreads = 256;
+constexpr int kThreads = 512;
 constexpr int kBufBytes = 48 * 1024;  // one staging buffer (keys + payload regions)
 
 struct SegParams {

@@ -148,6 +148,17 @@ __device__ __forceinline__ U to_ord(U x, const Xform& f) {
   const U m = (f.flt ? ashr : U(0)) | U(f.sign_or);
   return x ^ m ^ U(f.kdesc);
 }
+// Float keys, descending: ord'(x) = ~x ^ (ashr(x) | sign) -- one SHF + one
+// LOP3 -- and it is its own inverse.  (Callers branch on float+descending
+// once, outside their element loops.)
+template <class U>
+__device__ __forceinline__ U fdesc_ord(U x) {
+  using S = typename std::conditional<sizeof(U) == 4, int32_t, int64_t>::type;
+  constexpr U kSign = U(1) << (sizeof(U) * 8 - 1);
+  return U(~x) ^ (U(S(x) >> (sizeof(U) * 8 - 1)) | kSign);
+}
+__device__ __forceinline__ bool is_fdesc(const Xform& f) { return f.flt && f.kdesc; }
+
 template <class U>
 __device__ __forceinline__ U from_ord(U y, const Xform& f) {
   using S = typename std::conditional<sizeof(U) == 4, int32_t, int64_t>::type;

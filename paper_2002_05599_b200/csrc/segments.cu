@@ -267,14 +267,20 @@ __global__ void __launch_bounds__(kThreads, 2) seg_kernel(const SegParams prm) {
       // 16 bytes at a time over the whole staged chunk range (edge elements of
       // the neighbouring tiles are transformed too, but never stored)
       const int kchunks = int((uint64_t(e1) * sizeof(U) + 15) / 16 - (uint64_t(e0) * sizeof(U)) / 16);
+      const bool fd = is_fdesc(xf);
       for (int c = tid; c < kchunks; c += kThreads) {
         union {
           uint4 v;
           U e[16 / sizeof(U)];
         } u;
         u.v = reinterpret_cast<uint4*>(buf)[c];
+        if (fd) {
 #pragma unroll
-        for (int i = 0; i < int(16 / sizeof(U)); ++i) u.e[i] = to_ord<U>(u.e[i], xf);
+          for (int i = 0; i < int(16 / sizeof(U)); ++i) u.e[i] = fdesc_ord<U>(u.e[i]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < int(16 / sizeof(U)); ++i) u.e[i] = to_ord<U>(u.e[i], xf);
+        }
         reinterpret_cast<uint4*>(buf)[c] = u.v;
       }
       if constexpr (HAS_P) {
@@ -343,7 +349,10 @@ __global__ void __launch_bounds__(kThreads, 2) seg_kernel(const SegParams prm) {
     if (tid < 32) hist[tid] = 0;  // ready for the next call (after its leading sync)
     if (staged) {
       if (xf.active) {
-        store_range<U>(buf, kout, e0, e1, tid, [&](U k) { return from_ord<U>(k, xf); });
+        if (is_fdesc(xf))
+          store_range<U>(buf, kout, e0, e1, tid, [](U k) { return fdesc_ord<U>(k); });
+        else
+          store_range<U>(buf, kout, e0, e1, tid, [&](U k) { return from_ord<U>(k, xf); });
         if constexpr (HAS_P) store_range<P>(buf + G::K_REG, pout, e0, e1, tid, [&](P q) { return P(q ^ P(xf.pdesc)); });
       } else {
         store_range<U>(buf, kout, e0, e1, tid, [](U k) { return k; });

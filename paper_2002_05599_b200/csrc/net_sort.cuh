@@ -41,6 +41,9 @@
 #ifndef NSG_MAX_APL
 #define NSG_MAX_APL 16
 #endif
+#ifndef NSG_DEEP_MIN_ROW
+#define NSG_DEEP_MIN_ROW 32  // rows at least this long get the deep ring
+#endif
 
 namespace nsg {
 
@@ -161,8 +164,14 @@ struct NetCfg {
   using GK = RowGeom<N, KEB>;
   using GP = RowGeom<N, (PEB ? PEB : 4)>;
   static constexpr int ROW_BYTES = GK::R + (PEB ? GP::R : 0);
-  // ~NSG_TILE_BYTES of HBM bytes per warp per stage
-  static constexpr int APL_RAW = NSG_TILE_BYTES / (32 * ROW_BYTES);
+  // Rows of >= NSG_DEEP_MIN_ROW bytes use the "deep" configuration: 8 KiB
+  // tiles in a ~32 KiB per-warp ring, i.e. one 4-warp CTA streaming ~100 KiB
+  // per SM -- measured 4-13 % faster than 2-4 shallower CTAs for those rows
+  // (tools/variants.py sweeps).  Shorter rows keep 4 KiB
+  // tiles in a 3-deep ring (several CTAs per SM).
+  static constexpr bool DEEP = ROW_BYTES >= NSG_DEEP_MIN_ROW && NSG_STAGES == 3 && NSG_TILE_BYTES == 4096;
+  static constexpr int TILE_BYTES = DEEP ? 8192 : NSG_TILE_BYTES;
+  static constexpr int APL_RAW = TILE_BYTES / (32 * ROW_BYTES);
   static constexpr int APL_POW2 = APL_RAW >= 16 ? 16 : APL_RAW >= 8 ? 8 : APL_RAW >= 4 ? 4 : APL_RAW >= 2 ? 2 : 1;
   static constexpr int APL = APL_POW2 > NSG_MAX_APL ? NSG_MAX_APL : APL_POW2;
   static constexpr int ROWS = 32 * APL;
@@ -172,13 +181,8 @@ struct NetCfg {
   // ring depth and warps per CTA shrink for very long rows (n = 32 / 64)
   static constexpr int SMEM_BUDGET = 200 * 1024;
   static constexpr int STAGES_FIT = (SMEM_BUDGET / 2) / STAGE_SMEM;
-  // Rows of >= 128 B (one lane sorts one row per tile): a deep ring of ~32 KB
-  // per warp, i.e. one 4-warp CTA streaming ~100 KB per SM, measured 6-13 %
-  // faster than 2-3 shallower CTAs (tools/variants.py).
   static constexpr int DEEP_STAGES = (32 * 1024) / STAGE_SMEM;
-  static constexpr int WANT_STAGES =
-      (ROW_BYTES >= 128 && NSG_STAGES == 3) ? (DEEP_STAGES > 8 ? 8 : (DEEP_STAGES < 3 ? 3 : DEEP_STAGES))
-                                            : NSG_STAGES;
+  static constexpr int WANT_STAGES = DEEP ? (DEEP_STAGES > 8 ? 8 : (DEEP_STAGES < 3 ? 3 : DEEP_STAGES)) : NSG_STAGES;
   static constexpr int STAGES = WANT_STAGES <= STAGES_FIT ? WANT_STAGES : (STAGES_FIT >= 2 ? STAGES_FIT : 2);
   static constexpr int WARPS_FIT = SMEM_BUDGET / (STAGES * STAGE_SMEM);
   static constexpr int WARPS = WARPS_FIT >= NSG_WARPS ? NSG_WARPS : (WARPS_FIT >= 1 ? WARPS_FIT : 1);

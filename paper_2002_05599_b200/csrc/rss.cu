@@ -157,7 +157,8 @@ __device__ __forceinline__ void leaf_network(Elem<typename Cfg::Uk, typename Cfg
 }
 
 template <class U, class P, int NMAX, int DAG, int MODE, int LAYOUT>
-__global__ void __launch_bounds__(RssCfg<U, P, NMAX, DAG, MODE, LAYOUT>::WARPS * 32)
+__global__ void __launch_bounds__(RssCfg<U, P, NMAX, DAG, MODE, LAYOUT>::WARPS * 32,
+                                  NMAX <= 256 ? (IsNoPay<P>::value ? 6 : 3) : 2)
     rss_kernel(const RssParams prm) {
   using Cfg = RssCfg<U, P, NMAX, DAG, MODE, LAYOUT>;
   using E = Elem<U, P>;
@@ -349,15 +350,27 @@ __global__ void __launch_bounds__(RssCfg<U, P, NMAX, DAG, MODE, LAYOUT>::WARPS *
       const int lo = r_lo(e), cnt = r_cnt(e), buf = r_buf(e);
       const U* ks = wb.keys(buf) + lo;
       const P* ps = wb.pays(buf) + lo;
+      // Keys-only / UNIQUE: every leaf runs the 16-channel network padded with
+      // +inf sentinels (output is the unique order; no per-size divergence).
+      // REF mode: exact-size networks, except 11..15 of the best family which
+      // ARE restrictions of Green's 16 (DAG-exact when padded).
+      constexpr bool kPadAll = !std::is_same<typename Cfg::CX, CxRef>::value;
+      const bool pad16 = kPadAll || (DAG == 0 && cnt >= 11);
       E v[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         if (j < cnt) {
           v[j].k = ks[j];
           if constexpr (Cfg::HAS_P) v[j].p = ps[j];
+        } else {
+          v[j].k = U(~U(0));
+          if constexpr (Cfg::HAS_P) v[j].p = P(~P(0));
         }
       }
-      leaf_network<Cfg, DAG>(v, cnt);
+      if (pad16)
+        Net<DAG, 16>::template run<typename Cfg::CX>(v);
+      else
+        leaf_network<Cfg, DAG>(v, cnt);
       U* kd = wb.keys(0) + lo;
       P* pd = wb.pays(0) + lo;
 #pragma unroll

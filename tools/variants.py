@@ -23,11 +23,9 @@ sys.path.insert(0, str(ROOT))
 VARIANTS = {
     "base": (),
     "nonet": ("NSG_NO_NETWORK=1",),  # pipeline + smem transpose only: the kernel's memory ceiling
-    "st4": ("NSG_STAGES=4",),
-    "st6": ("NSG_STAGES=6",),
-    "st8": ("NSG_STAGES=8",),
-    "t8k_st4": ("NSG_TILE_BYTES=8192", "NSG_STAGES=4"),
-    "t2k_st8": ("NSG_TILE_BYTES=2048", "NSG_STAGES=8"),
+    "deep_all": ("NSG_DEEP_MIN_ROW=8",),
+    "deep_all_t8k": ("NSG_DEEP_MIN_ROW=8", "NSG_TILE_BYTES=8192"),
+    "deep64_t8k": ("NSG_DEEP_MIN_ROW=64", "NSG_TILE_BYTES=8192"),
 }
 CELLS = [(2, 8, 0), (3, 8, 0), (4, 8, 0), (8, 8, 0), (12, 8, 0), (16, 8, 0), (4, 8, 4), (16, 8, 4), (16, 8, 8),
          (8, 4, 0)]

@@ -169,7 +169,11 @@ struct NetCfg {
   // per SM -- measured 4-13 % faster than 2-4 shallower CTAs for those rows
   // (tools/variants.py sweeps).  Shorter rows keep 4 KiB
   // tiles in a 3-deep ring (several CTAs per SM).
-  static constexpr bool DEEP = ROW_BYTES >= NSG_DEEP_MIN_ROW && NSG_STAGES == 3 && NSG_TILE_BYTES == 4096;
+  // (merge configurations -- N = 32 or G > 1 -- are compute-heavy: they want
+  // warps, not depth, so they keep a 2-deep ring and several CTAs per SM)
+  static constexpr bool MERGE = N > 16 || G > 1;
+  static constexpr bool DEEP =
+      !MERGE && ROW_BYTES >= NSG_DEEP_MIN_ROW && NSG_STAGES == 3 && NSG_TILE_BYTES == 4096;
   static constexpr int TILE_BYTES = DEEP ? 8192 : NSG_TILE_BYTES;
   static constexpr int APL_RAW = TILE_BYTES / (32 * ROW_BYTES);
   static constexpr int APL_POW2 = APL_RAW >= 16 ? 16 : APL_RAW >= 8 ? 8 : APL_RAW >= 4 ? 4 : APL_RAW >= 2 ? 2 : 1;
@@ -182,7 +186,8 @@ struct NetCfg {
   static constexpr int SMEM_BUDGET = 200 * 1024;
   static constexpr int STAGES_FIT = (SMEM_BUDGET / 2) / STAGE_SMEM;
   static constexpr int DEEP_STAGES = (32 * 1024) / STAGE_SMEM;
-  static constexpr int WANT_STAGES = DEEP ? (DEEP_STAGES > 8 ? 8 : (DEEP_STAGES < 3 ? 3 : DEEP_STAGES)) : NSG_STAGES;
+  static constexpr int WANT_STAGES =
+      DEEP ? (DEEP_STAGES > 8 ? 8 : (DEEP_STAGES < 3 ? 3 : DEEP_STAGES)) : (MERGE ? 2 : NSG_STAGES);
   static constexpr int STAGES = WANT_STAGES <= STAGES_FIT ? WANT_STAGES : (STAGES_FIT >= 2 ? STAGES_FIT : 2);
   static constexpr int WARPS_FIT = SMEM_BUDGET / (STAGES * STAGE_SMEM);
   static constexpr int WARPS = WARPS_FIT >= NSG_WARPS ? NSG_WARPS : (WARPS_FIT >= 1 ? WARPS_FIT : 1);

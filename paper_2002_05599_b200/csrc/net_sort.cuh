@@ -67,17 +67,31 @@ struct NetParams {
 //    (8 consecutive chunks per quarter-warp) and the per-lane row reads
 //    (8 rows, same chunk) on 8 distinct bank groups, with no padding;
 //  * other even S: pad each row by 16 bytes (odd stride).
+//  * other even S (not a multiple of 16): XOR the chunk index with the low
+//    bits of its 128-byte line index,  phys = q ^ ((q >> 3) & (min(lowbit(S), 8) - 1))
+//    -- also a bijection, conflict-free for both patterns (checked
+//    exhaustively for every even S <= 64 that is not a multiple of 16);
+//  * remaining even S (multiples of 16 that are not powers of two): pad.
 template <int N, int EB>
 struct RowGeom {
   static constexpr int R = N * EB;  // row bytes in HBM
   static constexpr int V = (R % 16 == 0) ? 16 : ((R % 8 == 0) ? 8 : 4);
   static constexpr int S = R / 16;
-  static constexpr bool SWZ = (V == 16) && S >= 2 && (S & (S - 1)) == 0;
+  static constexpr bool POW2 = S >= 2 && (S & (S - 1)) == 0;
+  static constexpr int LOWBIT = S & -S;
+  static constexpr bool LSWZ = (V == 16) && !POW2 && (S % 2 == 0) && (S % 16 != 0);
+  static constexpr bool SWZ = (V == 16) && (POW2 || LSWZ);
   static constexpr bool PAD = (V == 16) && (S % 2 == 0) && !SWZ;
   static constexpr int RS = R + (PAD ? 16 : 0);  // row stride in smem
   static constexpr int W = R / 4;                // 32-bit words per row
 
-  __device__ __forceinline__ static int swz(int q) { return q ^ ((q / S) & 7); }
+  __device__ __forceinline__ static int swz(int q) {
+    if constexpr (POW2) {
+      return q ^ ((q / S) & 7);
+    } else {
+      return q ^ ((q >> 3) & ((LOWBIT < 8 ? LOWBIT : 8) - 1));
+    }
+  }
 
   // smem byte offset of the 16-byte chunk q of the contiguous tile
   __device__ __forceinline__ static int chunk_off(int q) {
@@ -295,19 +309,20 @@ __device__ __forceinline__ T shfl_xor_any(T v, int m) {
   }
 }
 
-// keep the partner's element o instead of a iff it is the min (keep_min) / max
+// keep the partner's element o instead of a iff it is the min (keep_min) / max.
+// One compare: take = (o < a) XOR !keep_min -- on a tie (o == a) the max side
+// takes o, which is the same value (identical key, or identical (key, payload)
+// in UNIQUE mode), so the result is unchanged.
 template <class Cfg>
 __device__ __forceinline__ void keep(Elem<typename Cfg::U, typename Cfg::P>& a,
                                      const Elem<typename Cfg::U, typename Cfg::P>& o, bool keep_min) {
-  bool olt, alt;
+  bool olt;
   if constexpr (Cfg::HAS_P) {
     olt = lex_lt(o.k, o.p, a.k, a.p);
-    alt = lex_lt(a.k, a.p, o.k, o.p);
   } else {
     olt = key_lt(o.k, a.k);
-    alt = key_lt(a.k, o.k);
   }
-  const bool take = keep_min ? olt : alt;
+  const bool take = olt != !keep_min;
   a.k = take ? o.k : a.k;
   if constexpr (Cfg::HAS_P) a.p = take ? o.p : a.p;
 }
@@ -332,7 +347,10 @@ __device__ __forceinline__ void merge_lanes(Elem<typename Cfg::U, typename Cfg::
   using E = Elem<typename Cfg::U, typename Cfg::P>;
   constexpr int G = Cfg::G, N = Cfg::N;
   const int gl = int(threadIdx.x) & (G - 1);
-#pragma unroll
+  // level and cross-lane stage loops stay rolled (their bodies differ only in
+  // the runtime lane mask), so the instruction footprint is one flip stage +
+  // one half-cleaner stage + one in-register merge, not log^2 copies
+#pragma unroll 1
   for (int m = 1; m < G; m <<= 1) {
     const bool flip_min = (gl & m) == 0;
 #pragma unroll
@@ -346,7 +364,7 @@ __device__ __forceinline__ void merge_lanes(Elem<typename Cfg::U, typename Cfg::
       const E o = shfl_elem<Cfg>(e[0], 2 * m - 1);
       keep<Cfg>(e[0], o, flip_min);
     }
-#pragma unroll
+#pragma unroll 1
     for (int j = m >> 1; j >= 1; j >>= 1) {
       const bool km = (gl & j) == 0;
 #pragma unroll

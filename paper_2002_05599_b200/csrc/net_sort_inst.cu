@@ -25,6 +25,9 @@ KernelInfo info() {
 }
 
 #if NSG_N == 0
+#ifndef NSG_MERGE_E_KEYS
+#define NSG_MERGE_E_KEYS 32  // items per lane, keys-only merge (16 or 32)
+#endif
 template <class U, class P, int E, int DAGM>
 KernelInfo merge_g(int g) {
   switch (g) {
@@ -67,17 +70,17 @@ KernelInfo lookup_dag(int key_bytes, int pay, int mode, int layout) {
 //  keys-only: E = 32 per lane (odd-even merge network, DAG 2), n = 32..1024;
 //  with payload: E = 16 per lane (Green-16), n = 32..512.
 KernelInfo merge_lookup(int n, int key_bytes, int pay, int* lanes_per_row) {
-  const int e = pay == 0 ? 32 : 16;
+  const int e = pay == 0 ? NSG_MERGE_E_KEYS : 16;
   if (n % e) return KernelInfo{};
   const int g = n / e;
   if (g < 1 || g > 32 || (g & (g - 1)) || (pay != 0 && g < 2)) return KernelInfo{};
   *lanes_per_row = g;
   if (key_bytes == 4) {
-    if (pay == 0) return merge_g<uint32_t, NoPay, 32, 2>(g);
+    if (pay == 0) return merge_g<uint32_t, NoPay, NSG_MERGE_E_KEYS, NSG_MERGE_E_KEYS == 32 ? 2 : 0>(g);
     if (pay == 1) return merge_g<uint32_t, uint32_t, 16, 0>(g);
     return merge_g<uint32_t, uint64_t, 16, 0>(g);
   }
-  if (pay == 0) return merge_g<uint64_t, NoPay, 32, 2>(g);
+  if (pay == 0) return merge_g<uint64_t, NoPay, NSG_MERGE_E_KEYS, NSG_MERGE_E_KEYS == 32 ? 2 : 0>(g);
   if (pay == 1) return merge_g<uint64_t, uint32_t, 16, 0>(g);
   return merge_g<uint64_t, uint64_t, 16, 0>(g);
 }

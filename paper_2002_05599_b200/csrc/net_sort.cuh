@@ -66,7 +66,6 @@ struct NetParams {
 //    16-byte chunk index q -- a bijection that keeps both the linear tile copy
 //    (8 consecutive chunks per quarter-warp) and the per-lane row reads
 //    (8 rows, same chunk) on 8 distinct bank groups, with no padding;
-//  * other even S: pad each row by 16 bytes (odd stride).
 //  * other even S (not a multiple of 16): XOR the chunk index with the low
 //    bits of its 128-byte line index,  phys = q ^ ((q >> 3) & (min(lowbit(S), 8) - 1))
 //    -- also a bijection, conflict-free for both patterns (checked

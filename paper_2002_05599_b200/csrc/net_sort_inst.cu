@@ -26,7 +26,7 @@ KernelInfo info() {
 
 #if NSG_N == 0
 #ifndef NSG_MERGE_E_KEYS
-#define NSG_MERGE_E_KEYS 32  // items per lane, keys-only merge (16 or 32)
+#define NSG_MERGE_E_KEYS 16  // items per lane, keys-only merge (16 measured faster than 32 for n >= 64)
 #endif
 template <class U, class P, int E, int DAGM>
 KernelInfo merge_g(int g) {

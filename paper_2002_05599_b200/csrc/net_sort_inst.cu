@@ -67,7 +67,8 @@ KernelInfo lookup_dag(int key_bytes, int pay, int mode, int layout) {
 
 #if NSG_N == 0
 // Merge sorter (kind MERGE), keys-only or UNIQUE (key, payload):
-//  keys-only: E = 32 per lane (odd-even merge network, DAG 2), n = 32..1024;
+//  keys-only: E = NSG_MERGE_E_KEYS per lane (16: Green-16, n = 32..512;
+//  32: the odd-even merge network of csrc/gen/nets.cuh, n = 32..1024);
 //  with payload: E = 16 per lane (Green-16), n = 32..512.
 KernelInfo merge_lookup(int n, int key_bytes, int pay, int* lanes_per_row) {
   const int e = pay == 0 ? NSG_MERGE_E_KEYS : 16;

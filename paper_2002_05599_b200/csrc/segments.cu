@@ -295,16 +295,26 @@ __global__ void __launch_bounds__(kThreads, 2) seg_kernel(const SegParams prm) {
         }
       }
     }
-    for (int s = a + tid; s < b; s += kThreads) {
-      const int len = int(offs[s + 1] - offs[s]);
-      if (len > 16) {
-        const uint32_t slot = atomicAdd(prm.long_count, 1u);
-        if (slot < prm.long_cap)
-          prm.long_ids[slot] = uint32_t(seg0 + s);
-        else
-          atomicAdd(prm.overflow, 1u);
-      } else if (len >= 2) {
-        atomicAdd(&hist[len], 1);
+    // each thread bins its SPT segments; the rank atomicAdd returns inside a
+    // length bin is kept in registers and placed after the scan
+    constexpr int SPT = (TS_ + kThreads - 1) / kThreads;
+    int lens[SPT], ranks[SPT];
+#pragma unroll
+    for (int i = 0; i < SPT; ++i) {
+      const int s = a + tid + i * kThreads;
+      lens[i] = 0;
+      if (s < b) {
+        const int len = int(offs[s + 1] - offs[s]);
+        if (len > 16) {
+          const uint32_t slot = atomicAdd(prm.long_count, 1u);
+          if (slot < prm.long_cap)
+            prm.long_ids[slot] = uint32_t(seg0 + s);
+          else
+            atomicAdd(prm.overflow, 1u);
+        } else if (len >= 2) {
+          lens[i] = len;
+          ranks[i] = atomicAdd(&hist[len], 1);
+        }
       }
     }
     __syncthreads();
@@ -322,20 +332,21 @@ __global__ void __launch_bounds__(kThreads, 2) seg_kernel(const SegParams prm) {
     }
     __syncthreads();
     const int nshort = hist[31];
-    for (int s = a + tid; s < b; s += kThreads) {
-      const int len = int(offs[s + 1] - offs[s]);
-      if (len >= 2 && len <= 16) perm[atomicAdd(&cur[len], 1)] = uint16_t(s - a);
-    }
+#pragma unroll
+    for (int i = 0; i < SPT; ++i)
+      if (lens[i]) perm[cur[lens[i]] + ranks[i]] = uint16_t(tid + i * kThreads);
     __syncthreads();
     if (staged) {
-      // warps pull 32-segment chunks, most expensive (longest) first, so the
-      // barrier after this loop waits for balanced work (LPT scheduling)
-      const int lane = tid & 31;
-      for (;;) {
-        int c = 0;
-        if (lane == 0) c = atomicAdd(&hist[30], 1);
-        c = __shfl_sync(0xffffffffu, c, 0);
-        if (c * 32 >= nshort) break;
+      // 32-segment chunks in descending cost order are dealt to the warps in
+      // snake order (w, then 2W-1-w, ...): a static longest-first schedule, so
+      // the barrier after this loop waits for balanced work without a shared
+      // work counter
+      constexpr int NW = kThreads / 32;
+      const int lane = tid & 31, w = tid >> 5;
+      const int nchunks = (nshort + 31) / 32;
+      for (int k = 0; k * NW < nchunks; ++k) {
+        const int c = k * NW + ((k & 1) ? (NW - 1 - w) : w);
+        if (c >= nchunks) continue;
         const int j = c * 32 + lane;
         if (j < nshort) {
           const int s = a + perm[j];

@@ -87,11 +87,12 @@ __device__ __forceinline__ void issue_range(unsigned char* dst, const unsigned c
   const uint64_t c0 = (uint64_t(e0) * EB) >> 4;
   const int nch = int(((uint64_t(e1) * EB + 15) >> 4) - c0);
   const unsigned char* gbase = src + (c0 << 4);
-  const int64_t lim = int64_t(limit_bytes) - int64_t(c0 << 4);  // bytes readable from gbase
+  const int64_t lim64 = int64_t(limit_bytes) - int64_t(c0 << 4);  // bytes readable from gbase
+  const int lim = lim64 < int64_t(nch) * 16 ? int(lim64) : nch * 16;
   for (int c = tid; c < nch; c += kThreads) {
     const int off = c << 4;
-    const int64_t rem = lim - off;
-    const int nb = rem >= 16 ? 16 : (rem > 0 ? int(rem) : 0);
+    const int rem = lim - off;
+    const int nb = rem >= 16 ? 16 : (rem > 0 ? rem : 0);
     cp_async16(dst + off, nb ? gbase + off : gbase, nb);
   }
 }
@@ -114,7 +115,7 @@ __device__ __forceinline__ void store_range(const unsigned char* sm, T* dst, uin
   uint64_t t_beg = b1 & ~uint64_t(15);
   if (t_beg < h_end) t_beg = h_end;
   unsigned char* g = reinterpret_cast<unsigned char*>(dst);
-  const int nhead = int((h_end - b0) / EB), ntail = int((b1 - t_beg) / EB);
+  const int nhead = int(h_end - b0) / EB, ntail = int(b1 - t_beg) / EB;
   if (tid < nhead) {
     const uint64_t b = b0 + uint64_t(tid) * EB;
     *reinterpret_cast<T*>(g + b) = f(*reinterpret_cast<const T*>(sm + (b - base)));
@@ -122,16 +123,18 @@ __device__ __forceinline__ void store_range(const unsigned char* sm, T* dst, uin
     const uint64_t b = t_beg + uint64_t(tid - 32) * EB;
     *reinterpret_cast<T*>(g + b) = f(*reinterpret_cast<const T*>(sm + (b - base)));
   }
-  for (uint64_t c = (h_end >> 4) + tid; c < (t_beg >> 4); c += kThreads) {
-    const uint64_t b = c << 4;
+  const int nmid = int(t_beg - h_end) >> 4;
+  const uint4* s16 = reinterpret_cast<const uint4*>(sm + (h_end - base));
+  unsigned char* g16 = g + h_end;
+  for (int c = tid; c < nmid; c += kThreads) {
     union {
       uint4 v;
       T e[16 / EB];
     } u;
-    u.v = *reinterpret_cast<const uint4*>(sm + (b - base));
+    u.v = s16[c];
 #pragma unroll
     for (int i = 0; i < 16 / EB; ++i) u.e[i] = f(u.e[i]);
-    stg128_cs(g + b, u.v);
+    stg128_cs(g16 + (c << 4), u.v);
   }
 }
 

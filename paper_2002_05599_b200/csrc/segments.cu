@@ -88,7 +88,11 @@ __device__ __forceinline__ void issue_range(unsigned char* dst, const unsigned c
   const int nch = int(((uint64_t(e1) * EB + 15) >> 4) - c0);
   const unsigned char* gbase = src + (c0 << 4);
   const int64_t lim64 = int64_t(limit_bytes) - int64_t(c0 << 4);  // bytes readable from gbase
-  const int lim = lim64 < int64_t(nch) * 16 ? int(lim64) : nch * 16;
+  if (lim64 >= int64_t(nch) * 16) {  // every chunk whole (all but the array's last tile)
+    for (int c = tid; c < nch; c += kThreads) cp_async16(dst + (c << 4), gbase + (c << 4), 16);
+    return;
+  }
+  const int lim = int(lim64);
   for (int c = tid; c < nch; c += kThreads) {
     const int off = c << 4;
     const int rem = lim - off;
@@ -242,17 +246,31 @@ __global__ void __launch_bounds__(kThreads, 2) seg_kernel(const SegParams prm) {
   const unsigned char* pin = static_cast<const unsigned char*>(prm.p_in);
   U* kout = static_cast<U*>(prm.k_out);
   P* pout = static_cast<P*>(prm.p_out);
-  const int64_t ntiles = (prm.nseg + TS_ - 1) / TS_;
-  const int64_t gstride = gridDim.x;
-  const uint32_t total = prm.offsets[prm.nseg];
+  const int64_t nseg = prm.nseg;
+  const int ntiles = int((nseg + TS_ - 1) / TS_);
+  const int gstride = int(gridDim.x);
+  const uint32_t total = prm.offsets[nseg];
   const uint64_t klimit = uint64_t(total) * sizeof(U), plimit = uint64_t(total) * G::PB;
+  // 16-byte offset copies when the offsets array is 16-byte aligned (a tile
+  // starts at a multiple of TS_ >= 512 offsets, so every tile is then aligned)
+  const bool offs16 = (reinterpret_cast<uintptr_t>(prm.offsets) & 15) == 0;
 
-  auto offs_slot = [&](int64_t k) { return reinterpret_cast<uint32_t*>(sm + G::OFF_OFFS) + (k % 3) * G::OFFS_STRIDE; };
-  auto data_slot = [&](int64_t k) { return sm + G::OFF_DATA + (k & 1) * G::BUF; };
-  auto nsegs_of = [&](int64_t t) { return int(prm.nseg - t * TS_ < TS_ ? prm.nseg - t * TS_ : TS_); };
-  auto issue_offs = [&](int64_t t, uint32_t* dst) {
+  auto offs_slot = [&](int k) { return reinterpret_cast<uint32_t*>(sm + G::OFF_OFFS) + (k % 3) * G::OFFS_STRIDE; };
+  auto data_slot = [&](int k) { return sm + G::OFF_DATA + (k & 1) * G::BUF; };
+  auto nsegs_of = [&](int t) { return int(nseg - int64_t(t) * TS_ < TS_ ? nseg - int64_t(t) * TS_ : TS_); };
+  auto issue_offs = [&](int t, uint32_t* dst) {
     const int nts = nsegs_of(t);
-    for (int i = tid; i <= nts; i += kThreads) cp_async4(dst + i, prm.offsets + t * TS_ + i);
+    const uint32_t* src = prm.offsets + int64_t(t) * TS_;
+    if (offs16) {  // nts + 1 offsets as 16-byte chunks, zero-filled past offsets[nseg]
+      const int nch = (nts + 4) >> 2;
+      if (tid < nch) {
+        const int rem = (nts + 1 - 4 * tid) * 4;
+        cp_async16(dst + 4 * tid, src + 4 * tid, rem >= 16 ? 16 : rem);
+      }
+      static_assert(TS_ / 4 + 1 <= kThreads, "one 16-byte offsets chunk per thread");
+    } else {
+      for (int i = tid; i <= nts; i += kThreads) cp_async4(dst + i, src + i);
+    }
   };
   auto issue_data = [&](unsigned char* buf, uint32_t e0, uint32_t e1) {
     issue_range<int(sizeof(U))>(buf, kin, e0, e1, klimit, tid);
@@ -376,7 +394,7 @@ __global__ void __launch_bounds__(kThreads, 2) seg_kernel(const SegParams prm) {
     // no trailing barrier: the next tile starts with wait + __syncthreads
   };
 
-  int64_t t = blockIdx.x;
+  int t = int(blockIdx.x);
   if (t >= ntiles) return;
   if (tid < 32) hist[tid] = 0;
   // prologue: offsets of tile 0 (synchronously), data of tile 0 + offsets of tile 1 (async)
@@ -391,13 +409,13 @@ __global__ void __launch_bounds__(kThreads, 2) seg_kernel(const SegParams prm) {
     if (t + gstride < ntiles) issue_offs(t + gstride, offs_slot(1));
     cp_async_commit();
   }
-  for (int64_t k = 0; t < ntiles; ++k, t += gstride) {
+  for (int k = 0; t < ntiles; ++k, t += gstride) {
     cp_async_wait<0>();
     __syncthreads();
     const uint32_t* offs = offs_slot(k);
     const int nts = nsegs_of(t);
     const bool fits = offs[nts] - offs[0] <= uint32_t(G::CAP);
-    const int64_t tn = t + gstride;
+    const int tn = t + gstride;
     if (tn < ntiles) {  // prefetch: data of the next tile, offsets of the one after
       const uint32_t* on = offs_slot(k + 1);
       const int ntn = nsegs_of(tn);
@@ -433,7 +451,7 @@ __global__ void __launch_bounds__(kThreads, 2) seg_kernel(const SegParams prm) {
         }
         __syncthreads();
       }
-      process(offs, a, b, t * TS_, buf, staged);
+      process(offs, a, b, int64_t(t) * TS_, buf, staged);
       a = b;
     }
   }

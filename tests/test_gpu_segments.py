@@ -139,3 +139,29 @@ def test_cfg4_full_size_properties(torch):
     ek, ep = oracle.typed_sort_segments(sub_off, w[off[lo]:off[hi]], ids[off[lo]:off[hi]], descending=True)
     assert np.array_equal(gk[off[lo]:off[hi]].cpu().numpy(), ek)
     assert np.array_equal(gp[off[lo]:off[hi]].cpu().numpy().view(np.uint32), ep)
+
+
+@pytest.mark.parametrize("shift", [1, 2, 3])
+def test_segments_unaligned_offsets(shift, torch):
+    """An offsets array that is not 16-byte aligned (a view into a larger
+    buffer) takes the 4-byte copy path; the aligned path zero-fills its last
+    16-byte chunk -- both must give the oracle's result."""
+    from paper_2002_05599_b200 import batch
+    rng = np.random.default_rng(20 + shift)
+    nseg = 4099 + shift
+    lengths = rng.integers(0, 14, nseg).astype(np.uint32)
+    off = _csr(lengths)
+    e = int(off[-1])
+    keys = rng.integers(0, 50, e).astype(np.uint32)
+    pay = np.arange(e, dtype=np.uint32)
+    dev = torch.device("cuda")
+    buf = torch.zeros(len(off) + shift, dtype=torch.int32, device=dev)
+    buf[shift:] = torch.from_numpy(off.view(np.int32)).to(dev)
+    ot = buf[shift:].view(torch.uint32)
+    assert ot.data_ptr() % 16 != 0
+    kt = torch.from_numpy(keys.view(np.int32)).to(dev).view(torch.uint32)
+    pt = torch.from_numpy(pay.view(np.int32)).to(dev).view(torch.uint32)
+    gk, gp = batch.sort_segments(ot, kt, pt, tie="unique")
+    ek, ep = oracle.typed_sort_segments(off, keys, pay, unique=True)
+    assert np.array_equal(gk.cpu().numpy().view(np.uint32), ek)
+    assert np.array_equal(gp.cpu().numpy().view(np.uint32), ep)

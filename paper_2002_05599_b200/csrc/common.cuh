@@ -151,11 +151,22 @@ __device__ __forceinline__ U to_ord(U x, const Xform& f) {
 // Float keys, descending: ord'(x) = ~x ^ (ashr(x) | sign) -- one SHF + one
 // LOP3 -- and it is its own inverse.  (Callers branch on float+descending
 // once, outside their element loops.)
+__device__ __forceinline__ uint32_t lop3_xnor_or(uint32_t a, uint32_t b, uint32_t c) {  // ~(a ^ (b | c))
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xe1;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
 template <class U>
 __device__ __forceinline__ U fdesc_ord(U x) {
-  using S = typename std::conditional<sizeof(U) == 4, int32_t, int64_t>::type;
-  constexpr U kSign = U(1) << (sizeof(U) * 8 - 1);
-  return U(~x) ^ (U(S(x) >> (sizeof(U) * 8 - 1)) | kSign);
+  // written as explicit LOP3s: left to itself the compiler emits the
+  // complement as a separate LOP3 (3 instructions per 32-bit word, not 2)
+  if constexpr (sizeof(U) == 4) {
+    return lop3_xnor_or(x, uint32_t(int32_t(x) >> 31), 0x80000000u);
+  } else {
+    const uint32_t lo = uint32_t(x), hi = uint32_t(x >> 32);
+    const uint32_t s = uint32_t(int32_t(hi) >> 31);
+    return (uint64_t(lop3_xnor_or(hi, s, 0x80000000u)) << 32) | lop3_xnor_or(lo, s, 0u);
+  }
 }
 __device__ __forceinline__ bool is_fdesc(const Xform& f) { return f.flt && f.kdesc; }
 

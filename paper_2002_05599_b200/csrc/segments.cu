@@ -5,15 +5,18 @@
 // length", done inside each CTA so the data is read from and written to HBM
 // exactly once:
 //
-//  1. a persistent CTA walks tiles of 512 consecutive segments.  The tile's
-//     offsets are prefetched two tiles ahead and its contiguous element range
-//     one tile ahead, with cp.async (16-byte chunks, any element alignment),
-//     into a double-buffered shared-memory ring -- the copy of tile i+1 is in
-//     flight while tile i is binned, sorted and stored;
+//  1. a persistent CTA (8 warps, 2 per SM) walks tiles of 1024 consecutive
+//     segments.  The tile's offsets are prefetched two tiles ahead and its
+//     contiguous element range one tile ahead, with cp.async (16-byte chunks,
+//     any element alignment), into a double-buffered shared-memory ring -- the
+//     copy of tile i+1 is in flight while tile i is binned, sorted and stored;
 //  2. segments are binned by exact length 2..16 with a shared-memory counting
-//     sort, so each warp runs ONE exact-length network (csrc/gen/nets.cuh)
-//     over 32 segments of (mostly) the same length -- no padding, so REF mode
-//     executes the reference's exact comparator DAG for that length;
+//     sort (longest first), and 32-segment chunks are dealt to the warps in
+//     snake order, so each warp runs one network over 32 segments of (mostly)
+//     the same length: the exact-length network (csrc/gen/nets.cuh) for 2..10,
+//     and for 11..16 the 16-channel network with +inf sentinels, which is the
+//     reference's exact DAG for the best family (see sort_segment_pad16) -- in
+//     REF mode for the Bose-Nelson family every length keeps its exact network;
 //  3. the tile is written back with 16-byte stores (element stores only for
 //     the two partial chunks shared with the neighbouring tiles);
 //  4. segments longer than 16 are appended to a device list and sorted by the
@@ -30,13 +33,26 @@ namespace nsg {
 
 namespace {
 
-// Large tiles (1024 segments, 8 warps): every length bin of the tile holds
-// enough segments that the 32-segment chunks are (nearly) single-length and
-// the per-tile sort work splits evenly over the warps.  Two staging buffers
-// of 48 KB -> 2 CTAs per SM.
-constexpr int kMaxTileSegs = 1024;
-constexpr int kThreads = 512;
-constexpr int kBufBytes = 48 * 1024;  // one staging buffer (keys + payload regions)
+// Large tiles (1024 segments): every length bin of the tile holds enough
+// segments that the 32-segment chunks are (nearly) single-length and the
+// per-tile sort work splits evenly over the warps.  Two staging buffers of
+// 48 KB -> 2 CTAs per SM.  8 warps per CTA: each warp's per-tile setup is
+// amortised over 128 segments (16 warps: 1.70 ms on cfg4, 8: 1.66, 4: 1.93).
+#ifndef NSG_SEG_THREADS
+#define NSG_SEG_THREADS 256  // 8 warps: measured best of 128/256/512 (cfg4)
+#endif
+#ifndef NSG_SEG_TILE
+#define NSG_SEG_TILE 1024
+#endif
+#ifndef NSG_SEG_BUF_KB
+#define NSG_SEG_BUF_KB 48
+#endif
+#ifndef NSG_SEG_MINB
+#define NSG_SEG_MINB 2
+#endif
+constexpr int kMaxTileSegs = NSG_SEG_TILE;
+constexpr int kThreads = NSG_SEG_THREADS;
+constexpr int kBufBytes = NSG_SEG_BUF_KB * 1024;  // one staging buffer (keys + payload regions)
 
 struct SegParams {
   const uint32_t* offsets;
@@ -230,7 +246,7 @@ __device__ __forceinline__ void sort_segment_smem(U* keys, P* pays, int len) {
 }
 
 template <class U, class P, int MODE, int DAG>
-__global__ void __launch_bounds__(kThreads, 2) seg_kernel(const SegParams prm) {
+__global__ void __launch_bounds__(kThreads, NSG_SEG_MINB) seg_kernel(const SegParams prm) {
   using G = SegGeom<U, P>;
   constexpr bool HAS_P = !IsNoPay<P>::value;
   using CX = typename std::conditional<!HAS_P, CxKeys,
@@ -263,11 +279,10 @@ __global__ void __launch_bounds__(kThreads, 2) seg_kernel(const SegParams prm) {
     const uint32_t* src = prm.offsets + int64_t(t) * TS_;
     if (offs16) {  // nts + 1 offsets as 16-byte chunks, zero-filled past offsets[nseg]
       const int nch = (nts + 4) >> 2;
-      if (tid < nch) {
-        const int rem = (nts + 1 - 4 * tid) * 4;
-        cp_async16(dst + 4 * tid, src + 4 * tid, rem >= 16 ? 16 : rem);
+      for (int c = tid; c < nch; c += kThreads) {
+        const int rem = (nts + 1 - 4 * c) * 4;
+        cp_async16(dst + 4 * c, src + 4 * c, rem >= 16 ? 16 : rem);
       }
-      static_assert(TS_ / 4 + 1 <= kThreads, "one 16-byte offsets chunk per thread");
     } else {
       for (int i = tid; i <= nts; i += kThreads) cp_async4(dst + i, src + i);
     }

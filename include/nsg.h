@@ -119,6 +119,32 @@ int nsg_classify_block(const uint64_t* keys, int64_t n, uint64_t s0, uint64_t s1
 /* Replaces `ns_lcg_next` (netsort_core.c:38-40) on the host. */
 uint32_t nsg_lcg_next(uint32_t seed);
 
+/* Replaces `ns_fill` (netsort_core.c:42-50) on DEVICE memory: item i gets
+ * key = the (2i+1)-th and ref = the (2i+2)-th minstd draw after `seed`,
+ * written as u64 at keys + i*key_stride_bytes and refs + i*ref_stride_bytes
+ * (either pointer may be NULL; stride 16 with refs = keys + 8 is the
+ * reference's item layout).  *final_state (host) receives the generator
+ * state after the 2n draws, as ns_fill returns it. */
+int nsg_fill_lcg(void* keys, int64_t key_stride_bytes, void* refs, int64_t ref_stride_bytes, int64_t n,
+                 uint32_t seed, uint32_t* final_state, void* stream);
+/* The generator state after k draws from `seed` (jump-ahead; host). */
+uint32_t nsg_lcg_jump(uint32_t seed, uint64_t k);
+
+/* Replaces `ns_fp_at` (netsort_core.c:70-79) on DEVICE keys: writes
+ * prod_i (z - key_i) mod (2^61 - 1) to *out (DEVICE).  Keys are unsigned
+ * 4- or 8-byte words at a byte stride (16 for the reference's items).  The
+ * z-bump search of ns_fp_search stays with the caller (retry with z + 1 while
+ * the value is 0).  `ws` >= nsg_fingerprint_ws_bytes() of device memory. */
+size_t nsg_fingerprint_ws_bytes(void);
+int nsg_fingerprint(const void* keys, int key_bytes, int64_t stride_bytes, int64_t n, uint64_t z, void* ws,
+                    size_t ws_bytes, unsigned long long* out, void* stream);
+/* Per-row fingerprints of a (rows, n) batch: out[r] (DEVICE) for row r. */
+int nsg_fingerprint_rows(const void* keys, int key_bytes, int64_t stride_bytes, int64_t rows, int64_t n,
+                         uint64_t z, unsigned long long* out, void* stream);
+/* Replaces `ns_scan_sorted` (netsort_core.c:95-100): *unsorted (DEVICE) = 0
+ * if keys[i-1] <= keys[i] (unsigned) for every i < n, else 1. */
+int nsg_scan_sorted(const void* keys, int key_bytes, int64_t stride_bytes, int64_t n, int* unsorted, void* stream);
+
 /* Seeded counter-based generator for synthetic batches (splitmix64 of
  * (seed, global index)), identical on every device and in oracle/. */
 int nsg_fill_splitmix(void* out, int64_t count, int elem_bytes, uint64_t seed, uint64_t first_index,

@@ -117,6 +117,42 @@ def lcg_next(s: int) -> int:
     return int(lib().or_lcg_next(s & 0xFFFFFFFF))
 
 
+def fill_items(arr: np.ndarray, seed: int) -> int:
+    """ns_fill (netsort_core.c:42-50), sequentially: key_i, ref_i are the
+    (2i+1)-th and (2i+2)-th draws; returns the final state."""
+    s = int(seed) & 0xFFFFFFFF
+    keys = np.empty(len(arr), dtype=np.uint64)
+    refs = np.empty(len(arr), dtype=np.uint64)
+    for i in range(len(arr)):
+        s = lcg_next(s)
+        keys[i] = s
+        s = lcg_next(s)
+        refs[i] = s
+    arr["key"], arr["ref"] = keys, refs
+    return s
+
+
+def lcg_jump(seed: int, k: int) -> int:
+    """The state after k draws: seed * 48271^k mod (2^31 - 1) (k >= 1)."""
+    return (int(seed) * pow(48271, int(k), 2147483647)) % 2147483647 if k else int(seed)
+
+
+FP_PRIME = (1 << 61) - 1
+
+
+def fingerprint(keys, z: int = 1) -> tuple:
+    """ns_fp_at / ns_fp_search (netsort_core.c:70-91) over python ints."""
+    keys = [int(k) % FP_PRIME for k in keys]
+    z = int(z)
+    while True:
+        zz, v = z % FP_PRIME, 1
+        for k in keys:
+            v = v * ((zz - k) % FP_PRIME) % FP_PRIME
+        if v:
+            return v, z
+        z += 1
+
+
 def _spec(kind: int, rss_cfg: str = "332", base: str = "net", threshold: int = 16, seed: int = 0x5EED,
           unique: bool = False) -> OrSpec:
     return OrSpec(kind, 0 if base == "net" else 1, int(rss_cfg[1]), threshold, seed, int(unique))

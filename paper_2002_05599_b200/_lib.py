@@ -30,6 +30,8 @@ EXPORTS = (
     "nsg_segments_ws_bytes", "nsg_sort_segments", "nsg_swap_pairs", "nsg_classify_block",
     "nsg_lcg_next", "nsg_fill_splitmix", "nsg_last_error", "nsg_version",
     "nsg_verify_rows", "nsg_verify_segments",
+    "nsg_fill_lcg", "nsg_lcg_jump", "nsg_fingerprint_ws_bytes", "nsg_fingerprint", "nsg_fingerprint_rows",
+    "nsg_scan_sorted",
 )
 
 
@@ -77,6 +79,14 @@ _SIGS = {
     "nsg_fill_splitmix": (ctypes.c_int, [_P, _I64, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, _P]),
     "nsg_verify_rows": (ctypes.c_int, [ctypes.POINTER(NsgSpec), _P, _P, _P, _P, _I64, _I64, _P, _P]),
     "nsg_verify_segments": (ctypes.c_int, [ctypes.POINTER(NsgSpec), _P, _I64, _P, _P, _P, _P, _P, _P]),
+    "nsg_fill_lcg": (ctypes.c_int, [_P, _I64, _P, _I64, _I64, ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint32),
+                                    _P]),
+    "nsg_lcg_jump": (ctypes.c_uint32, [ctypes.c_uint32, ctypes.c_uint64]),
+    "nsg_fingerprint_ws_bytes": (ctypes.c_size_t, []),
+    "nsg_fingerprint": (ctypes.c_int, [_P, ctypes.c_int, _I64, _I64, ctypes.c_uint64, _P, ctypes.c_size_t, _P,
+                                       _P]),
+    "nsg_fingerprint_rows": (ctypes.c_int, [_P, ctypes.c_int, _I64, _I64, _I64, ctypes.c_uint64, _P, _P]),
+    "nsg_scan_sorted": (ctypes.c_int, [_P, ctypes.c_int, _I64, _I64, _P, _P]),
     "nsg_last_error": (ctypes.c_char_p, []),
     "nsg_version": (ctypes.c_int, []),
 }

@@ -9,7 +9,8 @@ raises).  Functions keep the reference's names, arguments and error behaviour:
   run_sorter_many(spec, rows)          _native.pyx:190-208   <- the hot path
   swap_pairs(code, rows)               _native.pyx:211-220
   classify_block_u64(keys, s0,s1,s2,b) _native.pyx:223-235
-  lcg_next / fill_items / fingerprint / check_sorted   (host utilities)
+  lcg_next / fill_items / fingerprint / check_sorted   netsort_core.c:38-100 (on the device)
+  measure_array_in_row(spec, size, narrays, seed)      _native.pyx:285-308 (CUDA-event timed)
 
 `rows` may be a numpy `ITEM_DTYPE` array (host buffers; copies are pipelined
 with the sort inside the library) or a CUDA tensor of shape (m, n, 2) and
@@ -142,37 +143,87 @@ def lcg_stream(seed: int, count: int) -> np.ndarray:
     return out
 
 
-def fill_items(arr: np.ndarray, seed: int) -> int:
-    """ns_fill: key_i, ref_i from consecutive LCG draws; returns the final state."""
-    n = len(arr)
-    s = lcg_stream(seed, 2 * n)
-    arr["key"] = s[0::2]
-    arr["ref"] = s[1::2]
-    return int(s[-1]) if n else int(seed)
+def _items_on_device(arr, n=None):
+    """(CUDA (n, 2) u64 tensor of items, host array to copy back or None).
+
+    numpy ITEM_DTYPE arrays are staged to the device (the lane computes on the
+    GPU only); CUDA tensors whose last dimension is 2 (packed items) are used
+    in place."""
+    import torch
+    if _is_torch(arr):
+        if not arr.is_cuda or arr.dtype not in (torch.int64, torch.uint64) or arr.shape[-1] != 2 \
+                or not arr.is_contiguous():
+            raise ConfigurationError("expected a contiguous CUDA (..., 2) int64/uint64 tensor of packed items")
+        flat = arr.view(-1, 2)
+        nn = flat.shape[0] if n is None else int(n)
+        if nn > flat.shape[0]:
+            raise ConfigurationError(f"array holds {flat.shape[0]} items, need {nn}")
+        return flat[:nn], None
+    nn = len(arr) if n is None else int(n)
+    _check_items(arr, nn)
+    host = arr[:nn].view(np.uint64).reshape(nn, 2)
+    lib()
+    return torch.from_numpy(host.view(np.int64)).cuda(), host
 
 
-def _fp_once(keys, z: int, p: int) -> int:
-    v = 1
-    for k in keys:
-        v = (v * ((z - k) % p)) % p
-    return v
+def fill_items(arr, seed: int) -> int:
+    """ns_fill (netsort_core.c:42-50) on the device: key_i, ref_i from the
+    (2i+1)-th and (2i+2)-th LCG draws; returns the final generator state."""
+    import ctypes
+    import torch
+    l = lib()
+    if _is_torch(arr):
+        items, host = _items_on_device(arr)
+    else:
+        _check_items(arr, len(arr))
+        host = arr.view(np.uint64).reshape(len(arr), 2)
+        items = torch.empty((len(arr), 2), dtype=torch.int64, device="cuda")
+    n = items.shape[0]
+    final = ctypes.c_uint32(0)
+    ptr = items.data_ptr() if n else None
+    check(l.nsg_fill_lcg(ptr, 16, ptr + 8 if n else None, 16, n, int(seed) & 0xFFFFFFFF, ctypes.byref(final),
+                         current_stream_handle(items.device)))
+    if host is not None and n:
+        host[...] = items.cpu().numpy().view(np.uint64)
+    return int(final.value)
+
+
+def _fp_device(items, z: int, ws, out) -> int:
+    l = lib()
+    n = items.shape[0]
+    check(l.nsg_fingerprint(items.data_ptr() if n else None, 8, 16, n, int(z) & 0xFFFFFFFFFFFFFFFF,
+                            ws.data_ptr(), ws.numel(), out.data_ptr(), current_stream_handle(items.device)))
+    return int(out.item()) & 0xFFFFFFFFFFFFFFFF
 
 
 def fingerprint(arr, n=None, z=1, p=FP_PRIME) -> tuple:
-    """Multiset fingerprint prod(z - key) mod p with the z-bump search."""
-    n = len(arr) if n is None else n
-    keys = [int(k) for k in arr["key"][:n]]
+    """ns_fp_search (netsort_core.c:81-91): the first z' >= z whose multiset
+    fingerprint prod(z' - key) mod p is nonzero, and that value; computed on
+    the device (nsg_fingerprint), the z bump on the host as in the reference."""
+    import torch
+    if p != FP_PRIME:
+        raise ConfigurationError("the device lane fingerprints modulo FP_PRIME = 2^61 - 1 only")
+    items, _ = _items_on_device(arr, n)
+    ws = torch.empty(int(load_library().nsg_fingerprint_ws_bytes()), dtype=torch.uint8, device=items.device)
+    out = torch.empty(1, dtype=torch.int64, device=items.device)
+    z = int(z)
     while True:
-        v = _fp_once(keys, z % p, p)
+        v = _fp_device(items, z, ws, out)
         if v != 0:
             return v, z
         z += 1
 
 
 def check_sorted(arr, n=None) -> bool:
-    n = len(arr) if n is None else n
-    k = arr["key"][:n]
-    return bool(np.all(k[:-1] <= k[1:])) if n > 1 else True
+    """ns_scan_sorted (netsort_core.c:95-100) on the device."""
+    import torch
+    items, _ = _items_on_device(arr, n)
+    nn = items.shape[0]
+    if nn < 2:
+        return True
+    out = torch.empty(1, dtype=torch.int32, device=items.device)
+    check(lib().nsg_scan_sorted(items.data_ptr(), 8, 16, nn, out.data_ptr(), current_stream_handle(items.device)))
+    return int(out.item()) == 0
 
 
 def hybrid_stats(spec, arr):
@@ -180,8 +231,50 @@ def hybrid_stats(spec, arr):
 
 
 def measure_one_array_repeat(spec, size, iterations, seed):
-    raise ConfigurationError("OneArrayRepeat is a CPU cycle-count harness: use bench.py on the device lane")
+    raise ConfigurationError("OneArrayRepeat times one array per call on a CPU core: use measure_array_in_row "
+                             "(batched) on the device lane")
 
 
-def measure_array_in_row(spec, size, narrays, seed):
-    raise ConfigurationError("ArrayInRow is a CPU cycle-count harness: use bench.py on the device lane")
+def measure_array_in_row(spec, size, narrays, seed) -> int:
+    """ns_measure_air (netsort_core.c:606-659) on the device: fill
+    narrays*size items from the LCG (nsg_fill_lcg), sort a throwaway copy of
+    the first subarray (warm-up), then time ONE batched sort of all narrays
+    contiguous subarrays with CUDA events; returns nanoseconds (TIMER_KIND).
+
+    Verification replaces the std::sort reference copy: every subarray must be
+    non-decreasing by key and a permutation of its input (key, ref) pairs
+    (nsg_verify_rows, REF order) -- stronger than the reference's key equality
+    + per-array ref sum/xor.  Status mapping as the reference: a network with
+    size outside 2..16 (size >= 2) -> UnsupportedSize; a failed check ->
+    CorrectnessFailure(seed)."""
+    import torch
+    size, narrays = int(size), int(narrays)
+    if size < 1 or narrays < 1:
+        raise ConfigurationError("size and narrays must be >= 1")
+    if spec[0] == registry.KIND_NETWORK and size >= 2 and not 2 <= size <= 16:
+        raise UnsupportedSize("network sorters cover 2..16 items")
+    l = lib()
+    dev = torch.device("cuda")
+    big = torch.empty((narrays, size, 2), dtype=torch.int64, device=dev)
+    fill_items(big, seed)
+    inp = big.clone()
+    warm = big[:1].clone()
+    run_sorter_many(spec, warm)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record()
+    run_sorter_many(spec, big)
+    ev1.record()
+    ev1.synchronize()
+    ns = int(round(ev0.elapsed_time(ev1) * 1e6))
+    ki, pi = inp[..., 0].contiguous(), inp[..., 1].contiguous()
+    ko, po = big[..., 0].contiguous(), big[..., 1].contiguous()
+    order = registry.DeviceOrder(key_dtype=registry.KEY_U64, payload_dtype=registry.PAY_U64,
+                                 descending=0, tie_mode=registry.TIE_REF)
+    bad = torch.zeros(1, dtype=torch.int64, device=dev)
+    check(l.nsg_verify_rows(make_spec(spec, order), ki.data_ptr(), pi.data_ptr(), ko.data_ptr(), po.data_ptr(),
+                            narrays, size, bad.data_ptr(), current_stream_handle(dev)))
+    if int(bad.item()) != 0:
+        from .errors import CorrectnessFailure
+        raise CorrectnessFailure("sorted-check or fingerprint mismatch", seed=seed)
+    return ns

@@ -354,6 +354,57 @@ int nsg_fill_splitmix(void* out, int64_t count, int elem_bytes, uint64_t seed, u
 
 size_t nsg_segments_ws_bytes(int64_t nseg, int64_t nelem) { return segments_ws_bytes(nseg, nelem); }
 
+uint32_t nsg_lcg_jump(uint32_t seed, uint64_t k) { return lcg_jump(seed, k); }
+
+int nsg_fill_lcg(void* keys, int64_t key_stride_bytes, void* refs, int64_t ref_stride_bytes, int64_t n,
+                 uint32_t seed, uint32_t* final_state, void* stream) {
+  g_err.clear();
+  if (n < 0) return fail(NSG_ERR_SPEC, "negative length");
+  if ((keys && (key_stride_bytes < 8 || key_stride_bytes % 8 || reinterpret_cast<uintptr_t>(keys) % 8)) ||
+      (refs && (ref_stride_bytes < 8 || ref_stride_bytes % 8 || reinterpret_cast<uintptr_t>(refs) % 8)))
+    return fail(NSG_ERR_SPEC, "fill_lcg: 8-byte aligned u64 columns with strides that are multiples of 8");
+  if (final_state) *final_state = lcg_jump(seed, 2 * uint64_t(n));
+  if (n == 0 || (!keys && !refs)) return 0;
+  return launch_fill_lcg(keys, key_stride_bytes, refs, ref_stride_bytes, n, seed, static_cast<cudaStream_t>(stream));
+}
+
+static int check_key_column(const void* keys, int key_bytes, int64_t stride_bytes, int64_t n) {
+  if (key_bytes != 4 && key_bytes != 8) return fail(NSG_ERR_SPEC, "key_bytes must be 4 or 8");
+  if (n < 0) return fail(NSG_ERR_SPEC, "negative length");
+  if (n > 0 && (!keys || stride_bytes < key_bytes || stride_bytes % key_bytes ||
+                reinterpret_cast<uintptr_t>(keys) % key_bytes))
+    return fail(NSG_ERR_SPEC, "keys must be key_bytes-aligned with a stride that is a multiple of key_bytes");
+  return 0;
+}
+
+size_t nsg_fingerprint_ws_bytes(void) { return fingerprint_ws_bytes(); }
+
+int nsg_fingerprint(const void* keys, int key_bytes, int64_t stride_bytes, int64_t n, uint64_t z, void* ws,
+                    size_t ws_bytes, unsigned long long* out, void* stream) {
+  g_err.clear();
+  if (int rc = check_key_column(keys, key_bytes, stride_bytes, n)) return rc;
+  if (!ws || ws_bytes < fingerprint_ws_bytes() || !out)
+    return fail(NSG_ERR_SPEC, "fingerprint needs ws (nsg_fingerprint_ws_bytes) and a device output");
+  return launch_fingerprint(keys, key_bytes, stride_bytes, n, z, ws, out, static_cast<cudaStream_t>(stream));
+}
+
+int nsg_fingerprint_rows(const void* keys, int key_bytes, int64_t stride_bytes, int64_t rows, int64_t n,
+                         uint64_t z, unsigned long long* out, void* stream) {
+  g_err.clear();
+  if (rows < 0) return fail(NSG_ERR_SPEC, "negative row count");
+  if (int rc = check_key_column(keys, key_bytes, stride_bytes, rows * n)) return rc;
+  if (rows == 0) return 0;
+  if (!out) return fail(NSG_ERR_SPEC, "fingerprint_rows needs a device output");
+  return launch_fingerprint_rows(keys, key_bytes, stride_bytes, rows, n, z, out, static_cast<cudaStream_t>(stream));
+}
+
+int nsg_scan_sorted(const void* keys, int key_bytes, int64_t stride_bytes, int64_t n, int* unsorted, void* stream) {
+  g_err.clear();
+  if (int rc = check_key_column(keys, key_bytes, stride_bytes, n)) return rc;
+  if (!unsorted) return fail(NSG_ERR_SPEC, "scan_sorted needs a device output");
+  return launch_scan_sorted(keys, key_bytes, stride_bytes, n, unsorted, static_cast<cudaStream_t>(stream));
+}
+
 int nsg_verify_rows(const nsg_spec* sp, const void* keys_in, const void* pay_in, const void* keys_out,
                     const void* pay_out, int64_t rows, int64_t n, unsigned long long* bad_rows, void* stream) {
   g_err.clear();

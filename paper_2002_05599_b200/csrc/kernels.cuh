@@ -41,6 +41,17 @@ int launch_verify_rows(const nsg_spec& sp, const void* ki, const void* pi, const
 int launch_verify_segments(const nsg_spec& sp, const uint32_t* off, int64_t nseg, const void* ki, const void* pi,
                            const void* ko, const void* po, unsigned long long* bad, cudaStream_t st);
 
+// lane.cu
+uint32_t lcg_jump(uint32_t seed, uint64_t k);
+int launch_fill_lcg(void* keys, int64_t kstride, void* refs, int64_t rstride, int64_t n, uint32_t seed,
+                    cudaStream_t st);
+size_t fingerprint_ws_bytes();
+int launch_fingerprint(const void* keys, int kb, int64_t stride, int64_t n, uint64_t z, void* ws,
+                       unsigned long long* out, cudaStream_t st);
+int launch_fingerprint_rows(const void* keys, int kb, int64_t stride, int64_t rows, int64_t n, uint64_t z,
+                            unsigned long long* out, cudaStream_t st);
+int launch_scan_sorted(const void* keys, int kb, int64_t stride, int64_t n, int* unsorted, cudaStream_t st);
+
 // segments.cu
 size_t segments_ws_bytes(int64_t nseg, int64_t nelem);
 int launch_segments(const nsg_spec& sp, const uint32_t* offsets, int64_t nseg, const void* keys_in, void* keys_out,

@@ -495,7 +495,7 @@ def run_e2e(cells, batch, dev, world, rank, steps):
         dt = float(t.item())
     return {"value": world * arrays * steps / dt, "unit": "arrays/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "steps": steps,
-            "path": "batch.sort_rows(numpy pinned) -> nsg_sort_rows_host (chunked H2D/sort/D2H, 2 streams)"}
+            "path": "batch.sort_rows(numpy pinned) -> nsg_sort_rows_host (chunked H2D/sort/D2H, 3 streams)"}
 
 
 if __name__ == "__main__":

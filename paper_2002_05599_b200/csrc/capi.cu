@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -231,9 +232,10 @@ int nsg_run_sorter_many(const nsg_spec* sp, void* rows, int64_t m, int64_t n, vo
 // copy engines and the SMs overlap.  Device staging buffers are cached per
 // device and only grow.
 // ---------------------------------------------------------------------------
+constexpr int kPipeBufs = 3;  // H2D of chunk c+1 never waits for the D2H of chunk c-1
 struct HostPipe {
-  cudaStream_t s[2] = {nullptr, nullptr};
-  void* buf[2] = {nullptr, nullptr};
+  cudaStream_t s[kPipeBufs] = {};
+  void* buf[kPipeBufs] = {};
   size_t cap = 0;
 };
 static std::mutex g_pipe_mu;
@@ -243,24 +245,34 @@ static int get_pipe(size_t bytes_per_buf, HostPipe** out) {
   int dev = 0;
   NSG_CUDA(cudaGetDevice(&dev));
   HostPipe& p = g_pipes[dev];
-  if (!p.s[0]) {
-    NSG_CUDA(cudaStreamCreateWithFlags(&p.s[0], cudaStreamNonBlocking));
-    NSG_CUDA(cudaStreamCreateWithFlags(&p.s[1], cudaStreamNonBlocking));
-  }
+  if (!p.s[0])
+    for (int i = 0; i < kPipeBufs; ++i) NSG_CUDA(cudaStreamCreateWithFlags(&p.s[i], cudaStreamNonBlocking));
   if (p.cap < bytes_per_buf) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kPipeBufs; ++i) {
       if (p.buf[i]) NSG_CUDA(cudaFree(p.buf[i]));
       p.buf[i] = nullptr;
     }
     p.cap = 0;
-    for (int i = 0; i < 2; ++i) NSG_CUDA(cudaMalloc(&p.buf[i], bytes_per_buf));
+    for (int i = 0; i < kPipeBufs; ++i) NSG_CUDA(cudaMalloc(&p.buf[i], bytes_per_buf));
     p.cap = bytes_per_buf;
   }
   *out = &p;
   return 0;
 }
 
-static constexpr size_t kChunkBytes = size_t(64) << 20;
+static int sync_pipe(HostPipe* p) {
+  for (int i = 0; i < kPipeBufs; ++i) NSG_CUDA(cudaStreamSynchronize(p->s[i]));
+  return 0;
+}
+
+static size_t chunk_bytes() {
+  static const size_t v = [] {
+    const char* e = getenv("NSG_HOST_CHUNK_MB");
+    const long mb = e ? atol(e) : 0;
+    return size_t(mb > 0 ? mb : 64) << 20;
+  }();
+  return v;
+}
 
 int nsg_sort_rows_host(const nsg_spec* sp, const void* keys_in, void* keys_out, const void* pay_in,
                        void* pay_out, int64_t rows, int64_t n) {
@@ -272,7 +284,7 @@ int nsg_sort_rows_host(const nsg_spec* sp, const void* keys_in, void* keys_out, 
   const int pb = pay_bytes_of(sp->payload_dtype);
   const size_t row_k = size_t(n) * kb, row_p = size_t(n) * pb;
   // chunk rows so that each chunk is ~64 MiB and a multiple of 16 bytes per region
-  int64_t crow = std::max<int64_t>(1, int64_t(kChunkBytes / (row_k + row_p)));
+  int64_t crow = std::max<int64_t>(1, int64_t(chunk_bytes() / (row_k + row_p)));
   crow = (crow + 15) / 16 * 16;
   crow = std::min<int64_t>(crow, rows);
   const size_t kbytes_c = (size_t(crow) * row_k + 15) / 16 * 16;
@@ -287,8 +299,8 @@ int nsg_sort_rows_host(const nsg_spec* sp, const void* keys_in, void* keys_out, 
   int64_t c = 0;
   for (int64_t r0 = 0; r0 < rows; r0 += crow, ++c) {
     const int64_t rr = std::min<int64_t>(crow, rows - r0);
-    cudaStream_t s = p->s[c & 1];
-    char* dk = static_cast<char*>(p->buf[c & 1]);
+    cudaStream_t s = p->s[c % kPipeBufs];
+    char* dk = static_cast<char*>(p->buf[c % kPipeBufs]);
     char* dp = dk + kbytes_c;
     NSG_CUDA(cudaMemcpyAsync(dk, ki + size_t(r0) * row_k, size_t(rr) * row_k, cudaMemcpyHostToDevice, s));
     if (pb) NSG_CUDA(cudaMemcpyAsync(dp, pi + size_t(r0) * row_p, size_t(rr) * row_p, cudaMemcpyHostToDevice, s));
@@ -296,9 +308,7 @@ int nsg_sort_rows_host(const nsg_spec* sp, const void* keys_in, void* keys_out, 
     NSG_CUDA(cudaMemcpyAsync(ko + size_t(r0) * row_k, dk, size_t(rr) * row_k, cudaMemcpyDeviceToHost, s));
     if (pb) NSG_CUDA(cudaMemcpyAsync(po + size_t(r0) * row_p, dp, size_t(rr) * row_p, cudaMemcpyDeviceToHost, s));
   }
-  NSG_CUDA(cudaStreamSynchronize(p->s[0]));
-  NSG_CUDA(cudaStreamSynchronize(p->s[1]));
-  return 0;
+  return sync_pipe(p);
 }
 
 int nsg_run_sorter_many_host(const nsg_spec* sp, void* rows, int64_t m, int64_t n) {
@@ -308,7 +318,7 @@ int nsg_run_sorter_many_host(const nsg_spec* sp, void* rows, int64_t m, int64_t 
   if (sp->kind == NSG_KIND_NETWORK && n < 2) return 0;
   if (sp->kind == NSG_KIND_NETWORK && n > 16) return fail(NSG_ERR_SPEC, "network sorters cover 2..16 items");
   const size_t row_b = size_t(n) * 16;
-  int64_t crow = std::max<int64_t>(1, int64_t(kChunkBytes / row_b));
+  int64_t crow = std::max<int64_t>(1, int64_t(chunk_bytes() / row_b));
   crow = std::min<int64_t>(crow, m);
   std::lock_guard<std::mutex> lk(g_pipe_mu);
   HostPipe* p = nullptr;
@@ -317,15 +327,13 @@ int nsg_run_sorter_many_host(const nsg_spec* sp, void* rows, int64_t m, int64_t 
   int64_t c = 0;
   for (int64_t r0 = 0; r0 < m; r0 += crow, ++c) {
     const int64_t rr = std::min<int64_t>(crow, m - r0);
-    cudaStream_t s = p->s[c & 1];
-    char* d = static_cast<char*>(p->buf[c & 1]);
+    cudaStream_t s = p->s[c % kPipeBufs];
+    char* d = static_cast<char*>(p->buf[c % kPipeBufs]);
     NSG_CUDA(cudaMemcpyAsync(d, h + size_t(r0) * row_b, size_t(rr) * row_b, cudaMemcpyHostToDevice, s));
     if (int rc = nsg_run_sorter_many(sp, d, rr, n, s)) return rc;
     NSG_CUDA(cudaMemcpyAsync(h + size_t(r0) * row_b, d, size_t(rr) * row_b, cudaMemcpyDeviceToHost, s));
   }
-  NSG_CUDA(cudaStreamSynchronize(p->s[0]));
-  NSG_CUDA(cudaStreamSynchronize(p->s[1]));
-  return 0;
+  return sync_pipe(p);
 }
 
 int nsg_swap_pairs(int code, void* pairs, int64_t m, void* stream) {

@@ -35,6 +35,10 @@ def timeit(torch, fn, reps, warmup=3, flush=None):
     for _ in range(reps):
         if flush is not None:
             flush()
+        else:
+            # keep the GPU busy while the host enqueues the timed launch, so
+            # the start event does not absorb the Python call overhead
+            torch.cuda._sleep(200_000)
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         fn()
@@ -57,9 +61,14 @@ def main():
     dev = torch.device("cuda")
     pk = peak()
     flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush_rd = torch.zeros(64 << 20, dtype=torch.float32, device=dev)
 
     def flush():
+        # write 256 MiB (evicts the working set), then read 256 MiB so the L2
+        # holds clean unrelated lines: the timed launch neither hits in L2
+        # nor pays the write-back of the flush's dirty lines
         flush_buf.zero_()
+        flush_rd.sum()
 
     out = []
 

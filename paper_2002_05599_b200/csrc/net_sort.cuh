@@ -41,6 +41,12 @@
 #ifndef NSG_MAX_APL
 #define NSG_MAX_APL 16
 #endif
+#ifndef NSG_DEEP_WARPS
+#define NSG_DEEP_WARPS 4  // warps per CTA of the deep configuration (1 CTA per SM)
+#endif
+#ifndef NSG_DEEP_RING_KB
+#define NSG_DEEP_RING_KB 32  // per-warp ring of the deep configuration
+#endif
 #ifndef NSG_DEEP_MIN_ROW
 #define NSG_DEEP_MIN_ROW 32  // rows at least this long get the deep ring
 #endif
@@ -198,12 +204,13 @@ struct NetCfg {
   // ring depth and warps per CTA shrink for very long rows (n = 32 / 64)
   static constexpr int SMEM_BUDGET = 200 * 1024;
   static constexpr int STAGES_FIT = (SMEM_BUDGET / 2) / STAGE_SMEM;
-  static constexpr int DEEP_STAGES = (32 * 1024) / STAGE_SMEM;
+  static constexpr int DEEP_STAGES = (NSG_DEEP_RING_KB * 1024) / STAGE_SMEM;
   static constexpr int WANT_STAGES =
-      DEEP ? (DEEP_STAGES > 8 ? 8 : (DEEP_STAGES < 3 ? 3 : DEEP_STAGES)) : (MERGE ? 2 : NSG_STAGES);
+      DEEP ? (DEEP_STAGES > 8 ? 8 : (DEEP_STAGES < 2 ? 2 : DEEP_STAGES)) : (MERGE ? 2 : NSG_STAGES);
   static constexpr int STAGES = WANT_STAGES <= STAGES_FIT ? WANT_STAGES : (STAGES_FIT >= 2 ? STAGES_FIT : 2);
   static constexpr int WARPS_FIT = SMEM_BUDGET / (STAGES * STAGE_SMEM);
-  static constexpr int WARPS = WARPS_FIT >= NSG_WARPS ? NSG_WARPS : (WARPS_FIT >= 1 ? WARPS_FIT : 1);
+  static constexpr int WANT_WARPS = DEEP ? NSG_DEEP_WARPS : NSG_WARPS;
+  static constexpr int WARPS = WARPS_FIT >= WANT_WARPS ? WANT_WARPS : (WARPS_FIT >= 1 ? WARPS_FIT : 1);
   static constexpr int WARP_SMEM = STAGES * STAGE_SMEM;
   static constexpr int CTA_SMEM = WARPS * WARP_SMEM;
   using CX = typename std::conditional<!HAS_P, CxKeys,

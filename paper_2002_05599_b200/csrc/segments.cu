@@ -84,8 +84,7 @@ struct SegGeom {
   static constexpr int OFF_OFFS = 0;                                   // 3 slots
   static constexpr int OFF_PERM = OFF_OFFS + 3 * OFFS_STRIDE * 4;      // TS_ u16
   static constexpr int OFF_HIST = OFF_PERM + TS_ * 2;            // 32 int
-  static constexpr int OFF_CUR = OFF_HIST + 32 * 4;                    // 32 int
-  static constexpr int OFF_DATA = (OFF_CUR + 32 * 4 + 15) / 16 * 16;   // 2 buffers
+  static constexpr int OFF_DATA = (OFF_HIST + 32 * 4 + 15) / 16 * 16;  // 2 buffers
   static constexpr int SMEM = OFF_DATA + 2 * BUF;
 };
 
@@ -255,7 +254,6 @@ __global__ void __launch_bounds__(kThreads, NSG_SEG_MINB) seg_kernel(const SegPa
   extern __shared__ __align__(16) unsigned char sm[];
   uint16_t* perm = reinterpret_cast<uint16_t*>(sm + G::OFF_PERM);
   int* hist = reinterpret_cast<int*>(sm + G::OFF_HIST);
-  int* cur = reinterpret_cast<int*>(sm + G::OFF_CUR);
   const int tid = threadIdx.x;
   const Xform xf = prm.xf;
   const unsigned char* kin = static_cast<const unsigned char*>(prm.k_in);
@@ -354,23 +352,23 @@ __global__ void __launch_bounds__(kThreads, NSG_SEG_MINB) seg_kernel(const SegPa
       }
     }
     __syncthreads();
-    if (tid < 32) {  // exclusive scan over the length bins, LONGEST first
-      const int len = 16 - tid;
-      const int v = len >= 2 ? hist[len] : 0;
-      int incl = v;
+    // every warp scans the 15 bin counts itself (exclusive, LONGEST first:
+    // lane l holds bin 16 - l), so no barrier separates scan and placement
+    const int lane = tid & 31;
+    const int v = lane < 15 ? hist[16 - lane] : 0;
+    int incl = v;
 #pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, incl, d);
-        if (tid >= d) incl += t;
-      }
-      if (len >= 2) cur[len] = incl - v;
-      if (tid == 31) hist[31] = incl;
+    for (int d = 1; d < 32; d <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += t;
     }
-    __syncthreads();
-    const int nshort = hist[31];
+    const int excl = incl - v;
+    const int nshort = __shfl_sync(0xffffffffu, incl, 31);
 #pragma unroll
-    for (int i = 0; i < SPT; ++i)
-      if (lens[i]) perm[cur[lens[i]] + ranks[i]] = uint16_t(tid + i * kThreads);
+    for (int i = 0; i < SPT; ++i) {
+      const int start = __shfl_sync(0xffffffffu, excl, (16 - lens[i]) & 31);
+      if (lens[i]) perm[start + ranks[i]] = uint16_t(tid + i * kThreads);
+    }
     __syncthreads();
     if (staged) {
       // 32-segment chunks in descending cost order are dealt to the warps in
@@ -378,7 +376,7 @@ __global__ void __launch_bounds__(kThreads, NSG_SEG_MINB) seg_kernel(const SegPa
       // the barrier after this loop waits for balanced work without a shared
       // work counter
       constexpr int NW = kThreads / 32;
-      const int lane = tid & 31, w = tid >> 5;
+      const int w = tid >> 5;
       const int nchunks = (nshort + 31) / 32;
       for (int k = 0; k * NW < nchunks; ++k) {
         const int c = k * NW + ((k & 1) ? (NW - 1 - w) : w);

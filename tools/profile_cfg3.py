@@ -1,5 +1,5 @@
-"""One launch each of the cfg3 sorters (for ncu): merge n=128, merge n=256,
-RSS 332 n=64 -- 2^20 arrays of int64 keys."""
+"""One launch each of the cfg3 merge sorters (for ncu): n = 64, 128, 256 --
+2^20 arrays of int64 keys."""
 
 import sys
 from pathlib import Path
@@ -12,7 +12,7 @@ def main():
 
     from paper_2002_05599_b200 import batch
     dev = torch.device("cuda")
-    for kind, n in (("merge", 128), ("merge", 256), ("rss", 64)):
+    for kind, n in (("merge", 64), ("merge", 128), ("merge", 256)):
         x = torch.randint(-2**63, 2**63 - 1, (1 << 20, n), dtype=torch.int64, device=dev)
         y, _ = batch.sort_rows(x, kind=kind)
         torch.cuda.synchronize()

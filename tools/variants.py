@@ -22,13 +22,12 @@ sys.path.insert(0, str(ROOT))
 
 VARIANTS = {
     "base": (),
-    "nonet": ("NSG_NO_NETWORK=1",),  # pipeline + smem transpose only: the kernel's memory ceiling
-    "deep_all": ("NSG_DEEP_MIN_ROW=8",),
-    "deep_all_t8k": ("NSG_DEEP_MIN_ROW=8", "NSG_TILE_BYTES=8192"),
-    "deep64_t8k": ("NSG_DEEP_MIN_ROW=64", "NSG_TILE_BYTES=8192"),
+    "dw8_r16": ("NSG_DEEP_WARPS=8", "NSG_DEEP_RING_KB=16"),
+    "dw8_r24": ("NSG_DEEP_WARPS=8", "NSG_DEEP_RING_KB=24"),
+    "dw6_r32": ("NSG_DEEP_WARPS=6", "NSG_DEEP_RING_KB=32"),
 }
-CELLS = [(2, 8, 0), (3, 8, 0), (4, 8, 0), (8, 8, 0), (12, 8, 0), (16, 8, 0), (4, 8, 4), (16, 8, 4), (16, 8, 8),
-         (8, 4, 0)]
+CELLS = [(2, 8, 0), (3, 8, 0), (4, 8, 0), (5, 8, 0), (6, 8, 0), (8, 8, 0), (12, 8, 0), (16, 8, 0), (4, 8, 4),
+         (5, 8, 4), (16, 8, 4), (16, 8, 8), (8, 4, 0)]
 
 
 def build_all():
@@ -71,6 +70,7 @@ def time_one(lib):
         ts = []
         for _ in range(7):
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda._sleep(200_000)  # host enqueue latency stays outside the events
             s.record()
             run()
             e.record()
@@ -86,7 +86,7 @@ if __name__ == "__main__":
     if sys.argv[1] == "build":
         build_all()
     elif sys.argv[1] == "time":
-        for name in VARIANTS:
+        for name in list(VARIANTS) + ["base"]:  # base twice: the spread is the noise floor
             lib = ROOT / "variants" / name / "libnsg.so"
             subprocess.run([sys.executable, __file__, "one", str(lib)], check=False)
     elif sys.argv[1] == "one":

@@ -160,6 +160,17 @@ __device__ __forceinline__ void word_put(uint32_t* w, int j, uint64_t v) {
   w[2 * j + 1] = uint32_t(v >> 32);
 }
 
+// Deep-configuration shapes measured faster with 8 warps x 16 KiB rings than
+// with 4 warps x 32 KiB (tools/variants.py, profiles/round1/deep_warps.md):
+// rows whose shared-memory transpose + network is long enough that one warp
+// per scheduler cannot hide it.  (N, key bytes, payload bytes.)  The u32
+// n = 8 shape also measured faster at 2^24 rows but not at cfg1's 2^20 (a
+// 64 MiB launch is ramp-bound, 17-19.5 us either way), so it stays at 4.
+constexpr bool deep8_shape(int n, int keb, int peb) {
+  return (keb == 8 && peb == 0 && (n == 5 || n == 6 || n == 7 || n == 11 || n == 13 || n == 14)) ||
+         (keb == 8 && peb == 4 && (n == 3 || n == 5 || n == 9 || n == 10 || n == 15));
+}
+
 // Compile-time configuration of one kernel instance.  G > 1 (merge sorter):
 // a row of G*N items is split into G contiguous sub-rows of N, one per lane;
 // each lane sorts its sub-row with Net<DAG, N>, then the G lanes merge with
@@ -204,12 +215,13 @@ struct NetCfg {
   // ring depth and warps per CTA shrink for very long rows (n = 32 / 64)
   static constexpr int SMEM_BUDGET = 200 * 1024;
   static constexpr int STAGES_FIT = (SMEM_BUDGET / 2) / STAGE_SMEM;
-  static constexpr int DEEP_STAGES = (NSG_DEEP_RING_KB * 1024) / STAGE_SMEM;
+  static constexpr bool DEEP8 = DEEP && NSG_DEEP_WARPS == 4 && NSG_DEEP_RING_KB == 32 && deep8_shape(N, KEB, PEB);
+  static constexpr int DEEP_STAGES = ((DEEP8 ? 16 : NSG_DEEP_RING_KB) * 1024) / STAGE_SMEM;
   static constexpr int WANT_STAGES =
       DEEP ? (DEEP_STAGES > 8 ? 8 : (DEEP_STAGES < 2 ? 2 : DEEP_STAGES)) : (MERGE ? 2 : NSG_STAGES);
   static constexpr int STAGES = WANT_STAGES <= STAGES_FIT ? WANT_STAGES : (STAGES_FIT >= 2 ? STAGES_FIT : 2);
   static constexpr int WARPS_FIT = SMEM_BUDGET / (STAGES * STAGE_SMEM);
-  static constexpr int WANT_WARPS = DEEP ? NSG_DEEP_WARPS : NSG_WARPS;
+  static constexpr int WANT_WARPS = DEEP ? (DEEP8 ? 8 : NSG_DEEP_WARPS) : NSG_WARPS;
   static constexpr int WARPS = WARPS_FIT >= WANT_WARPS ? WANT_WARPS : (WARPS_FIT >= 1 ? WARPS_FIT : 1);
   static constexpr int WARP_SMEM = STAGES * STAGE_SMEM;
   static constexpr int CTA_SMEM = WARPS * WARP_SMEM;

@@ -23,11 +23,8 @@ sys.path.insert(0, str(ROOT))
 VARIANTS = {
     "base": (),
     "dw8_r16": ("NSG_DEEP_WARPS=8", "NSG_DEEP_RING_KB=16"),
-    "dw8_r24": ("NSG_DEEP_WARPS=8", "NSG_DEEP_RING_KB=24"),
-    "dw6_r32": ("NSG_DEEP_WARPS=6", "NSG_DEEP_RING_KB=32"),
 }
-CELLS = [(2, 8, 0), (3, 8, 0), (4, 8, 0), (5, 8, 0), (6, 8, 0), (8, 8, 0), (12, 8, 0), (16, 8, 0), (4, 8, 4),
-         (5, 8, 4), (16, 8, 4), (16, 8, 8), (8, 4, 0)]
+CELLS = [(n, 8, pb) for n in range(2, 17) for pb in (0, 4)] + [(8, 4, 0), (16, 8, 8)]  # cfg2 + cfg1/cfg5 shapes
 
 
 def build_all():
@@ -86,7 +83,7 @@ if __name__ == "__main__":
     if sys.argv[1] == "build":
         build_all()
     elif sys.argv[1] == "time":
-        for name in list(VARIANTS) + ["base"]:  # base twice: the spread is the noise floor
+        for name in list(VARIANTS) + list(VARIANTS):  # twice: the spread is the noise floor
             lib = ROOT / "variants" / name / "libnsg.so"
             subprocess.run([sys.executable, __file__, "one", str(lib)], check=False)
     elif sys.argv[1] == "one":

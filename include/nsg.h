@@ -90,11 +90,15 @@ int nsg_sort_rows_host(const nsg_spec* sp, const void* keys_in, void* keys_out, 
 
 /* Segmented (CSR) batch: segment s = [offsets[s], offsets[s+1]) of keys /
  * payloads; lengths 0..16 are sorted by the exact-length network of the spec's
- * family; longer segments by the warp RSS sorter.  `ws` is a device workspace
- * of nsg_segments_ws_bytes(nseg, nelem) bytes. */
+ * family; lengths 17..1024 by the warp RSS sorter.  `ws` is a device workspace
+ * of nsg_segments_ws_bytes(nseg, nelem) bytes.  Segments longer than 1024
+ * items are NOT sorted: they are counted in the workspace, and
+ * nsg_segments_check(ws) (which synchronises the stream) reports them as
+ * NSG_ERR_SPEC -- call it unless every segment is known to be <= 1024. */
 size_t nsg_segments_ws_bytes(int64_t nseg, int64_t nelem);
 int nsg_sort_segments(const nsg_spec* sp, const uint32_t* offsets, int64_t nseg, const void* keys_in,
                       void* keys_out, const void* pay_in, void* pay_out, void* ws, size_t ws_bytes, void* stream);
+int nsg_segments_check(const void* ws, void* stream);
 
 /* On-device verification (the reference's sorted scan + multiset check,
  * netsort_core.c:56-100,642-657): counts into *bad_rows (DEVICE memory) the

@@ -18,6 +18,7 @@ import numpy as np
 from . import networks as nw
 from . import registry
 from ._lib import check, current_stream_handle, lib, make_spec
+from ._lib import check as _check
 from .errors import ConfigurationError
 from .registry import DeviceOrder
 
@@ -138,8 +139,13 @@ def verify_segments(offsets, keys_in, keys_out, payload_in=None, payload_out=Non
 
 def sort_segments(offsets, keys, payload=None, *, family: str = "best", swap: str = "4CmS",
                   descending: bool = False, tie: str = "unique", out_keys=None, out_payload=None,
-                  workspace=None):
-    """Sort CSR segments [offsets[s], offsets[s+1]) of keys (+payload), on device."""
+                  workspace=None, check: bool = True):
+    """Sort CSR segments [offsets[s], offsets[s+1]) of keys (+payload), on device.
+
+    Segments of up to 1024 items are supported; with `check` (default) the
+    call synchronises and raises ConfigurationError if a longer one was
+    present (it is left unsorted).  `check=False` keeps the call fully
+    asynchronous for callers that bound their segment lengths."""
     import torch
     if not _is_torch(keys) or not keys.is_cuda:
         host = True
@@ -166,7 +172,9 @@ def sort_segments(offsets, keys, payload=None, *, family: str = "best", swap: st
                              pay_t.data_ptr() if pay_t is not None else None,
                              op.data_ptr() if op is not None else None, ws.data_ptr(), ws_bytes,
                              current_stream_handle(keys_t.device))
-    check(rc, network=False)
+    _check(rc, network=False)
+    if check or host:
+        _check(l.nsg_segments_check(ws.data_ptr(), current_stream_handle(keys_t.device)))
     if host:
         return ok.cpu().numpy(), (op.cpu().numpy() if op is not None else None)
     return ok, op

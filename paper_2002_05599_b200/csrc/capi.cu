@@ -444,4 +444,16 @@ int nsg_sort_segments(const nsg_spec* sp, const uint32_t* offsets, int64_t nseg,
                          static_cast<cudaStream_t>(stream));
 }
 
+int nsg_segments_check(const void* ws, void* stream) {
+  g_err.clear();
+  if (!ws) return fail(NSG_ERR_SPEC, "segments_check needs the workspace of nsg_sort_segments");
+  uint32_t words[2] = {0, 0};  // [long segment count, segments > 1024 left unsorted]
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  NSG_CUDA(cudaMemcpyAsync(words, ws, sizeof(words), cudaMemcpyDeviceToHost, st));
+  NSG_CUDA(cudaStreamSynchronize(st));
+  if (words[1])
+    return fail(NSG_ERR_SPEC, "%u segment(s) longer than 1024 items were left unsorted (device limit)", words[1]);
+  return 0;
+}
+
 }  // extern "C"

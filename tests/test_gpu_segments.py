@@ -165,3 +165,19 @@ def test_segments_unaligned_offsets(shift, torch):
     ek, ep = oracle.typed_sort_segments(off, keys, pay, unique=True)
     assert np.array_equal(gk.cpu().numpy().view(np.uint32), ek)
     assert np.array_equal(gp.cpu().numpy().view(np.uint32), ep)
+
+
+def test_segments_longer_than_1024_fail_loudly(torch):
+    """Segments > 1024 items are beyond the device sorters: the call raises
+    (nsg_segments_check) instead of returning unsorted data silently."""
+    from paper_2002_05599_b200 import batch
+    from paper_2002_05599_b200.errors import ConfigurationError
+    off = _csr(np.array([5, 1025, 3], dtype=np.uint32))
+    keys = np.arange(int(off[-1]), dtype=np.uint32)[::-1].copy()
+    with pytest.raises(ConfigurationError, match="longer than 1024"):
+        _run(torch, off, keys, None)
+    off = _csr(np.array([5, 1024, 3], dtype=np.uint32))
+    keys = np.arange(int(off[-1]), dtype=np.uint32)[::-1].copy()
+    gk, _ = _run(torch, off, keys, None)
+    ek, _ = oracle.typed_sort_segments(off, keys, None)
+    assert np.array_equal(gk, ek)

@@ -23,6 +23,8 @@
 //
 // UNIQUE mode (typed batches with payload) classifies by key exactly the same
 // way and orders leaves lexicographically by (key, payload).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "gen/nets.cuh"
 #include "kernels.cuh"
@@ -48,8 +50,12 @@ constexpr LcgPow make_lcg_pow() {
 }
 __constant__ LcgPow c_lcg_pow = make_lcg_pow();
 
-__device__ __forceinline__ uint32_t lcg_jump(uint32_t s, int j) {  // lcg^j(s)
-  return uint32_t((uint64_t(s) * c_lcg_pow.p[j]) % kLcgM);
+__device__ __forceinline__ uint32_t lcg_jump(uint32_t s, int j) {  // lcg^j(s), j >= 1
+  // s * 48271^j mod (2^31 - 1) by Mersenne folding (no 64-bit division)
+  const uint64_t x = uint64_t(s) * c_lcg_pow.p[j];  // < 2^63
+  uint64_t r = (x & kLcgM) + (x >> 31);             // < 3 * 2^31
+  r = (r & kLcgM) + (r >> 31);                      // <= M + 2
+  return uint32_t(r >= kLcgM ? r - kLcgM : r);
 }
 
 struct RssParams {
@@ -269,10 +275,19 @@ __global__ void __launch_bounds__(RssCfg<U, P, NMAX, DAG, MODE, LAYOUT>::WARPS *
       state = lcg_jump(state, sample);
       // rank among the sample (ties broken by draw index -> a total order)
       int ra = 0, rb = 0;
-      for (int u = 0; u < sample; ++u) {
-        const U ku = u < 32 ? __shfl_sync(0xffffffffu, s_a, u) : __shfl_sync(0xffffffffu, s_b, u - 32);
-        ra += (ku < s_a) || (ku == s_a && u < lane);
-        rb += (ku < s_b) || (ku == s_b && u < lane + 32);
+      if (sample <= 32) {  // every config up to a = 8: one key per lane
+        // (ku, u) < (s_a, lane) as one borrow chain; sample is a multiple of 4
+#pragma unroll 4
+        for (int u = 0; u < sample; ++u) {
+          const U ku = __shfl_sync(0xffffffffu, s_a, u);
+          ra += lex_lt(ku, uint32_t(u), s_a, uint32_t(lane));
+        }
+      } else {
+        for (int u = 0; u < sample; ++u) {
+          const U ku = u < 32 ? __shfl_sync(0xffffffffu, s_a, u) : __shfl_sync(0xffffffffu, s_b, u - 32);
+          ra += (ku < s_a) || (ku == s_a && u < lane);
+          rb += (ku < s_b) || (ku == s_b && u < lane + 32);
+        }
       }
       if (has_a) smp[ra] = s_a;
       if (has_b) smp[rb] = s_b;
@@ -444,12 +459,299 @@ __global__ void __launch_bounds__(RssCfg<U, P, NMAX, DAG, MODE, LAYOUT>::WARPS *
   }
 }
 
+// ---------------------------------------------------------------------------
+// Thread-per-array RSS for short rows (n <= NT).  The warp kernel above runs
+// every node's control flow once per warp, so for n <= 64 most of its issue
+// slots are spent on one array's scalar bookkeeping.  Here each THREAD runs
+// the reference recursion (ns_rss_rec) sequentially on its own array --
+// literally the reference's loop structure: draws in order, sample sorted,
+// stable counting scatter, recursion depth-first, base case exact networks --
+// with per-thread arrays interleaved in shared memory (element i of thread t
+// at [i * TPB + t], so the 32 lanes of a warp touch 32 consecutive words).
+// Rows are staged with coalesced cooperative loads/stores.
+// ---------------------------------------------------------------------------
+template <class U, class P, int NT, int TPB>
+struct TCfg {
+  static constexpr bool HAS_P = !IsNoPay<P>::value;
+  static constexpr int PB = PayBytes<P>::value;
+  static constexpr int OFF_K = 0;                                           // 2 x NT x TPB keys
+  static constexpr int OFF_P = OFF_K + 2 * NT * TPB * int(sizeof(U));       // 2 x NT x TPB payloads
+  static constexpr int OFF_STK = OFF_P + 2 * NT * TPB * PB;                 // NT/2 x TPB ranges
+  static constexpr int OFF_TAG = OFF_STK + NT / 2 * TPB * 4;                // NT x TPB tags
+  static constexpr int SMEM = OFF_TAG + NT * TPB;
+};
+
+template <class U, class P, int NT, int TPB, int DAG, int MODE, int LAYOUT>
+__global__ void __launch_bounds__(TPB) rss_thread_kernel(const RssParams prm) {
+  using C = TCfg<U, P, NT, TPB>;
+  using CX = typename std::conditional<!C::HAS_P, CxKeys,
+                                       typename std::conditional<MODE == MODE_REF, CxRef, CxUnique>::type>::type;
+  using E = Elem<U, P>;
+  constexpr bool HAS_P = C::HAS_P;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  U* K = reinterpret_cast<U*>(smem_raw + C::OFF_K);
+  P* PP = reinterpret_cast<P*>(smem_raw + C::OFF_P);
+  uint32_t* STK = reinterpret_cast<uint32_t*>(smem_raw + C::OFF_STK);
+  uint8_t* TAG = smem_raw + C::OFF_TAG;
+  const int t = threadIdx.x;
+  const int n = prm.n;
+  const Xform xf = prm.xf;
+  const int a = prm.oversampling, sample = 4 * a;
+  const float inv_n = 1.0f / float(n);
+  auto kat = [&](int b, int i) -> U& { return K[(b * NT + i) * TPB + t]; };
+  auto pat = [&](int b, int i) -> P& { return PP[(b * NT + i) * TPB + t]; };
+  auto less = [&](U bk, const P& bp, U ak, const P& ap) {
+    if constexpr (HAS_P && MODE == MODE_UNIQUE) return bk < ak || (bk == ak && bp < ap);
+    else return bk < ak;
+  };
+  // leaf [lo, lo+cnt) of buffer `buf`, sorted into buffer 0
+  auto leaf = [&](int lo, int cnt, int buf, bool net) {
+    if (cnt < 2) {
+      if (cnt == 1 && buf) {
+        kat(0, lo) = kat(1, lo);
+        if constexpr (HAS_P) pat(0, lo) = pat(1, lo);
+      }
+      return;
+    }
+    if (net && prm.base_kind == 0 && cnt <= 16) {
+      // ns_small_base network: exact size in REF mode (11..15 of the best
+      // family are restrictions of Green-16, so padded is DAG-exact);
+      // keys-only / UNIQUE: padded 16 (unique output, no divergence)
+      constexpr bool kPadAll = !std::is_same<CX, CxRef>::value;
+      E v[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (j < cnt) {
+          v[j].k = kat(buf, lo + j);
+          if constexpr (HAS_P) v[j].p = pat(buf, lo + j);
+        } else {
+          v[j].k = U(~U(0));
+          if constexpr (HAS_P) v[j].p = P(~P(0));
+        }
+      }
+      if (kPadAll || (DAG == 0 && cnt >= 11)) {
+        Net<DAG, 16>::template run<CX>(v);
+      } else {
+        switch (cnt) {
+          case 2: Net<DAG, 2>::template run<CX>(v); break;
+          case 3: Net<DAG, 3>::template run<CX>(v); break;
+          case 4: Net<DAG, 4>::template run<CX>(v); break;
+          case 5: Net<DAG, 5>::template run<CX>(v); break;
+          case 6: Net<DAG, 6>::template run<CX>(v); break;
+          case 7: Net<DAG, 7>::template run<CX>(v); break;
+          case 8: Net<DAG, 8>::template run<CX>(v); break;
+          case 9: Net<DAG, 9>::template run<CX>(v); break;
+          case 10: Net<DAG, 10>::template run<CX>(v); break;
+          case 11: Net<DAG, 11>::template run<CX>(v); break;
+          case 12: Net<DAG, 12>::template run<CX>(v); break;
+          case 13: Net<DAG, 13>::template run<CX>(v); break;
+          case 14: Net<DAG, 14>::template run<CX>(v); break;
+          case 15: Net<DAG, 15>::template run<CX>(v); break;
+          default: Net<DAG, 16>::template run<CX>(v); break;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (j < cnt) {
+          kat(0, lo + j) = v[j].k;
+          if constexpr (HAS_P) pat(0, lo + j) = v[j].p;
+        }
+      }
+      return;
+    }
+    // stable insertion sort (ns_ins_def, netsort_core.c:124-134) in place
+    for (int i = 1; i < cnt; ++i) {
+      const U vk = kat(buf, lo + i);
+      P vp{};
+      if constexpr (HAS_P) vp = pat(buf, lo + i);
+      int j = i - 1;
+      while (j >= 0) {
+        const U ak = kat(buf, lo + j);
+        P ap{};
+        if constexpr (HAS_P) ap = pat(buf, lo + j);
+        if (!less(vk, vp, ak, ap)) break;
+        kat(buf, lo + j + 1) = ak;
+        if constexpr (HAS_P) pat(buf, lo + j + 1) = ap;
+        --j;
+      }
+      kat(buf, lo + j + 1) = vk;
+      if constexpr (HAS_P) pat(buf, lo + j + 1) = vp;
+    }
+    if (buf)
+      for (int i = 0; i < cnt; ++i) {
+        kat(0, lo + i) = kat(1, lo + i);
+        if constexpr (HAS_P) pat(0, lo + i) = pat(1, lo + i);
+      }
+  };
+
+  for (int64_t row0 = int64_t(blockIdx.x) * TPB; row0 < prm.rows; row0 += int64_t(gridDim.x) * TPB) {
+    const int nrows = int(prm.rows - row0 < TPB ? prm.rows - row0 : TPB);
+    const int total = nrows * n;
+    // ---- coalesced load into the interleaved layout (ordered-key space) ----
+    for (int e = t; e < total; e += TPB) {
+      const int r = int((float(e) + 0.5f) * inv_n);
+      const int i = e - r * n;
+      const int64_t g = row0 * n + e;
+      U k;
+      P p{};
+      if constexpr (LAYOUT == LAYOUT_AOS16) {
+        const uint4 it = static_cast<const uint4*>(prm.k_in)[g];
+        k = U(uint64_t(it.x) | (uint64_t(it.y) << 32));
+        if constexpr (HAS_P) p = P(uint64_t(it.z) | (uint64_t(it.w) << 32));
+      } else {
+        k = static_cast<const U*>(prm.k_in)[g];
+        if (xf.active) k = to_ord<U>(k, xf);
+        if constexpr (HAS_P) {
+          p = static_cast<const P*>(prm.p_in)[g];
+          if (xf.active) p ^= P(xf.pdesc);
+        }
+      }
+      K[i * TPB + r] = k;
+      if constexpr (HAS_P) PP[i * TPB + r] = p;
+    }
+    __syncthreads();
+    if (t < nrows) {
+      // ---- ns_rss_rec (netsort_core.c:325-391), depth first ----------------
+      int sp = 0;
+      auto push = [&](int lo, int cnt, int depth, int buf) {
+        STK[sp * TPB + t] = uint32_t(lo) | (uint32_t(cnt) << 8) | (uint32_t(depth) << 16) | (uint32_t(buf) << 24);
+        ++sp;
+      };
+      uint32_t state = prm.seed;
+      push(0, n, 0, 0);
+      while (sp > 0) {
+        --sp;
+        const uint32_t e = STK[sp * TPB + t];
+        const int lo = int(e & 255u), cnt = int((e >> 8) & 255u), depth = int((e >> 16) & 255u),
+                  buf = int(e >> 24);
+        if (cnt <= prm.threshold) {
+          leaf(lo, cnt, buf, true);
+          continue;
+        }
+        if (cnt < sample) {
+          leaf(lo, cnt, buf, cnt <= 16);
+          continue;
+        }
+        if (depth >= 64 || sample > 64) {
+          leaf(lo, cnt, buf, false);
+          continue;
+        }
+        // sample of 4a keys at positions state^(t+1) % cnt, sorted
+        U s0, s1, s2;
+        if (sample <= 16) {
+          Elem<U, NoPay> v[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            if (q < sample) {
+              state = lcg_jump(state, 1);
+              v[q].k = kat(buf, lo + int(state % uint32_t(cnt)));
+            } else {
+              v[q].k = U(~U(0));
+            }
+          }
+          Net<DAG, 16>::template run<CxKeys>(v);
+          s0 = v[0].k, s1 = v[0].k, s2 = v[0].k;
+#pragma unroll
+          for (int q = 1; q < 16; ++q) {
+            if (q == a - 1) s0 = v[q].k;
+            if (q == 2 * a - 1) s1 = v[q].k;
+            if (q == 3 * a - 1) s2 = v[q].k;
+          }
+        } else {
+          U smp[64];
+          for (int q = 0; q < sample; ++q) {
+            state = lcg_jump(state, 1);
+            U k = kat(buf, lo + int(state % uint32_t(cnt)));
+            int j = q - 1;
+            while (j >= 0 && k < smp[j]) {
+              smp[j + 1] = smp[j];
+              --j;
+            }
+            smp[j + 1] = k;
+          }
+          s0 = smp[a - 1];
+          s1 = smp[2 * a - 1];
+          s2 = smp[3 * a - 1];
+        }
+        // classify (NS_CLS_LANE) + count
+        int c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+        for (int i = 0; i < cnt; ++i) {
+          const U k = kat(buf, lo + i);
+          const bool c = s1 < k;
+          const U x = c ? s2 : s0;
+          const int tag = (int(c) << 1) + int(x < k);
+          TAG[(lo + i) * TPB + t] = uint8_t(tag);
+          c0 += tag == 0;
+          c1 += tag == 1;
+          c2 += tag == 2;
+          c3 += tag == 3;
+        }
+        if (max(max(c0, c1), max(c2, c3)) == cnt) {  // no progress possible
+          leaf(lo, cnt, buf, false);
+          continue;
+        }
+        // stable counting scatter into the other buffer
+        const int ob = buf ^ 1;
+        int o0 = 0, o1 = c0, o2 = c0 + c1, o3 = c0 + c1 + c2;
+        for (int i = 0; i < cnt; ++i) {
+          const int tag = TAG[(lo + i) * TPB + t];
+          const int pos = tag == 0 ? o0 : tag == 1 ? o1 : tag == 2 ? o2 : o3;
+          o0 += tag == 0;
+          o1 += tag == 1;
+          o2 += tag == 2;
+          o3 += tag == 3;
+          kat(ob, lo + pos) = kat(buf, lo + i);
+          if constexpr (HAS_P) pat(ob, lo + pos) = pat(buf, lo + i);
+        }
+        // children 3..0 pushed so bucket 0 is processed first
+        const int cs[4] = {c0, c1, c2, c3};
+        const int st[4] = {0, c0, c0 + c1, c0 + c1 + c2};
+#pragma unroll
+        for (int b = 3; b >= 0; --b) {
+          if (cs[b] > 1)
+            push(lo + st[b], cs[b], depth + 1, ob);
+          else if (cs[b] == 1)
+            leaf(lo + st[b], 1, ob, true);
+        }
+      }
+    }
+    __syncthreads();
+    // ---- coalesced store --------------------------------------------------
+    for (int e = t; e < total; e += TPB) {
+      const int r = int((float(e) + 0.5f) * inv_n);
+      const int i = e - r * n;
+      const int64_t g = row0 * n + e;
+      U k = K[i * TPB + r];
+      P p{};
+      if constexpr (HAS_P) p = PP[i * TPB + r];
+      if constexpr (LAYOUT == LAYOUT_AOS16) {
+        static_cast<uint4*>(prm.k_out)[g] =
+            make_uint4(uint32_t(uint64_t(k)), uint32_t(uint64_t(k) >> 32), uint32_t(uint64_t(p)),
+                       uint32_t(uint64_t(p) >> 32));
+      } else {
+        if (xf.active) k = from_ord<U>(k, xf);
+        static_cast<U*>(prm.k_out)[g] = k;
+        if constexpr (HAS_P) {
+          if (xf.active) p ^= P(xf.pdesc);
+          static_cast<P*>(prm.p_out)[g] = p;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 struct RssKernel {
   const void* fn;
   int smem;
   int threads;
-  int warps;
+  int warps;  // arrays per CTA
 };
+
+bool env_flag_set(const char* name) {  // A/B switch for the warp kernel (tests, tuning)
+  const char* e = getenv(name);
+  return e && e[0] && e[0] != '0';
+}
 
 template <class U, class P, int NMAX, int DAG, int MODE, int LAYOUT>
 RssKernel rss_info_n() {
@@ -477,6 +779,42 @@ RssKernel rss_pick_dag(int key_bytes, int pay, int mode, int layout) {
                 : rss_info_n<uint64_t, uint32_t, NMAX, DAG, MODE_REF, LAYOUT_SOA>();
   return mode ? rss_info_n<uint64_t, uint64_t, NMAX, DAG, MODE_UNIQUE, LAYOUT_SOA>()
               : rss_info_n<uint64_t, uint64_t, NMAX, DAG, MODE_REF, LAYOUT_SOA>();
+}
+
+template <class U, class P, int NT, int DAG, int MODE, int LAYOUT>
+RssKernel rss_thread_info() {
+  constexpr int TPB = 64;
+  return {reinterpret_cast<const void*>(&rss_thread_kernel<U, P, NT, TPB, DAG, MODE, LAYOUT>),
+          TCfg<U, P, NT, TPB>::SMEM, TPB, TPB};
+}
+
+template <int NT, int DAG>
+RssKernel rss_thread_pick_dag(int key_bytes, int pay, int mode, int layout) {
+  if (layout == LAYOUT_AOS16)
+    return mode ? rss_thread_info<uint64_t, uint64_t, NT, DAG, MODE_UNIQUE, LAYOUT_AOS16>()
+                : rss_thread_info<uint64_t, uint64_t, NT, DAG, MODE_REF, LAYOUT_AOS16>();
+  if (key_bytes == 4) {
+    if (pay == 0) return rss_thread_info<uint32_t, NoPay, NT, DAG, MODE_UNIQUE, LAYOUT_SOA>();
+    if (pay == 1)
+      return mode ? rss_thread_info<uint32_t, uint32_t, NT, DAG, MODE_UNIQUE, LAYOUT_SOA>()
+                  : rss_thread_info<uint32_t, uint32_t, NT, DAG, MODE_REF, LAYOUT_SOA>();
+    return mode ? rss_thread_info<uint32_t, uint64_t, NT, DAG, MODE_UNIQUE, LAYOUT_SOA>()
+                : rss_thread_info<uint32_t, uint64_t, NT, DAG, MODE_REF, LAYOUT_SOA>();
+  }
+  if (pay == 0) return rss_thread_info<uint64_t, NoPay, NT, DAG, MODE_UNIQUE, LAYOUT_SOA>();
+  if (pay == 1)
+    return mode ? rss_thread_info<uint64_t, uint32_t, NT, DAG, MODE_UNIQUE, LAYOUT_SOA>()
+                : rss_thread_info<uint64_t, uint32_t, NT, DAG, MODE_REF, LAYOUT_SOA>();
+  return mode ? rss_thread_info<uint64_t, uint64_t, NT, DAG, MODE_UNIQUE, LAYOUT_SOA>()
+              : rss_thread_info<uint64_t, uint64_t, NT, DAG, MODE_REF, LAYOUT_SOA>();
+}
+
+// rows of n <= 32 items: thread-per-array kernel (38-70 KB per 64 arrays).
+// At n = 64 the doubled buffers leave 4 warps per SM and it measured 1.8x
+// SLOWER than the warp kernel (5.4 vs 2.95 ms on cfg3), so 33.. stay there.
+RssKernel rss_thread_pick(int dag, int key_bytes, int pay, int mode, int layout) {
+  return dag ? rss_thread_pick_dag<32, 1>(key_bytes, pay, mode, layout)
+             : rss_thread_pick_dag<32, 0>(key_bytes, pay, mode, layout);
 }
 
 RssKernel rss_pick(int n, int dag, int key_bytes, int pay, int mode, int layout) {
@@ -519,7 +857,9 @@ int launch_rss(const nsg_spec& sp, const void* k_in, void* k_out, const void* p_
   prm.seg_off = seg_off;
   prm.seg_count = seg_count;
   prm.seg_overflow = seg_overflow;
-  const RssKernel k = rss_pick(int(n), sp.family == 0 ? 0 : 1, key_bytes, pay, mode, layout);
+  const bool per_thread = !seg_ids && n <= 32 && !env_flag_set("NSG_RSS_WARP_ONLY");
+  const RssKernel k = per_thread ? rss_thread_pick(sp.family == 0 ? 0 : 1, key_bytes, pay, mode, layout)
+                                 : rss_pick(int(n), sp.family == 0 ? 0 : 1, key_bytes, pay, mode, layout);
   int sms = 0, occ = 0;
   if (int rc = kernel_residency(k.fn, k.threads, k.smem, &occ, &sms)) return rc;
   const int64_t need = (rows + k.warps - 1) / k.warps;

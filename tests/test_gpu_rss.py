@@ -1,4 +1,5 @@
-"""GPU parity of Register Sample Sort (warp-per-array kernel) vs the oracle.
+"""GPU parity of Register Sample Sort (thread-per-array kernel for n <= 32,
+warp-per-array kernel above) vs the oracle.
 
 REF mode is bit-exact with the reference including payload order under key
 ties, because the kernel replays the reference's LCG draws in depth-first
@@ -55,7 +56,7 @@ def test_rss_random_vs_oracle(cfg, base, torch):
     kind_base = "ins" if base.startswith("IS") else "net"
     if base.startswith("SN"):
         fam = {"Best": "best", "BN-L": "bn-l", "BN-P": "bn-p", "BN-R": "bn-r"}[base.split()[1]]
-    for n in (2, 16, 17, 20, 35, 64, 100, 255, 256, 257, 700, 1024):
+    for n in (2, 16, 17, 20, 24, 31, 32, 33, 35, 64, 100, 255, 256, 257, 700, 1024):
         for gen in ("u64", "dup", "few", "sorted", "rev", "equal"):
             m = 64
             if gen == "u64":
@@ -156,3 +157,31 @@ def test_cfg3_full_size_distributions(n, torch):
     ek, _ = oracle.typed_sort_rows(sub, None, kind="rss")
     k, _ = batch.sort_rows(uni[:512].contiguous(), kind="rss")
     assert np.array_equal(k.cpu().numpy(), ek)
+
+
+@pytest.mark.parametrize("mode", ["ref_items", "unique_typed"])
+def test_rss_thread_and_warp_kernels_agree(mode, torch, monkeypatch):
+    """n <= 32 runs the thread-per-array kernel; NSG_RSS_WARP_ONLY=1 forces the
+    warp kernel on the same rows: both must equal the oracle bit for bit."""
+    from paper_2002_05599_b200 import backend, batch, registry
+    rng = np.random.default_rng(99)
+    spec = registry.spec_rss("332", "SN Best 4CmS")
+    for n in (17, 23, 32):
+        keys = rng.integers(0, 5, size=(301, n), dtype=np.uint64)
+        refs = np.arange(keys.size, dtype=np.uint64).reshape(keys.shape)
+        outs = []
+        for warp_only in ("0", "1"):
+            monkeypatch.setenv("NSG_RSS_WARP_ONLY", warp_only)
+            if mode == "ref_items":
+                got = _items(keys, refs)
+                backend.run_sorter_many(spec, got)
+                outs.append(got)
+            else:
+                k, p = batch.sort_rows(keys.astype(np.int64), refs.astype(np.uint32), kind="rss", tie="unique")
+                outs.append((k, p))
+        if mode == "ref_items":
+            exp = _items(keys, refs)
+            oracle.run_items(exp, kind="rss", family="best", rss_cfg="332", base="net")
+            assert np.array_equal(outs[0], exp) and np.array_equal(outs[1], exp), n
+        else:
+            assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1]), n

@@ -104,8 +104,8 @@ struct RssCfg {
   static constexpr int OFF_A = 0;
   static constexpr int OFF_B = BUF_BYTES;
   static constexpr int OFF_STACK = 2 * BUF_BYTES;              // NMAX/2 u32
-  static constexpr int OFF_LEAF = OFF_STACK + NMAX / 2 * 4;    // NMAX u32
-  static constexpr int OFF_SMP = OFF_LEAF + NMAX * 4;          // 64 keys
+  static constexpr int OFF_LEAF = OFF_STACK + NMAX / 2 * 4;    // 2 x NMAX u32 (leaf lists)
+  static constexpr int OFF_SMP = OFF_LEAF + 2 * NMAX * 4;      // 64 keys
   static constexpr int WARP_SMEM = (OFF_SMP + 64 * 8 + 15) / 16 * 16;
   static constexpr int CTA_SMEM = WARPS * WARP_SMEM;
   using CX = typename std::conditional<!HAS_P, CxKeys,
@@ -159,6 +159,38 @@ __device__ __forceinline__ void leaf_network(Elem<typename Cfg::Uk, typename Cfg
     case 15: Net<DAG, 15>::template run<CX>(v); break;
     case 16: Net<DAG, 16>::template run<CX>(v); break;
     default: break;
+  }
+}
+
+// One leaf of c <= M items (c == 0: idle lane) through the M-channel
+// network with +inf sentinels, from its buffer into buffer A.  Keys-only /
+// UNIQUE mode only (the padded network's output is the unique order).
+template <class Cfg, int DAG, int M>
+__device__ __forceinline__ void leaf_pad(const WarpBufs<Cfg>& wb, int lo, int c, int b) {
+  using U = typename Cfg::Uk;
+  using P = typename Cfg::Pk;
+  const U* ks = wb.keys(b) + lo;
+  const P* ps = wb.pays(b) + lo;
+  Elem<U, P> v[M];
+#pragma unroll
+  for (int j = 0; j < M; ++j) {
+    if (j < c) {
+      v[j].k = ks[j];
+      if constexpr (Cfg::HAS_P) v[j].p = ps[j];
+    } else {
+      v[j].k = U(~U(0));
+      if constexpr (Cfg::HAS_P) v[j].p = P(~P(0));
+    }
+  }
+  Net<DAG, M>::template run<typename Cfg::CX>(v);
+  U* kd = wb.keys(0) + lo;
+  P* pd = wb.pays(0) + lo;
+#pragma unroll
+  for (int j = 0; j < M; ++j) {
+    if (j < c) {
+      kd[j] = v[j].k;
+      if constexpr (Cfg::HAS_P) pd[j] = v[j].p;
+    }
   }
 }
 
@@ -216,18 +248,27 @@ __global__ void __launch_bounds__(RssCfg<U, P, NMAX, DAG, MODE, LAYOUT>::WARPS *
     }
     uint32_t* stk = wb.stack();
     uint32_t* leaf = wb.leaves();
-    int sp = 0;          // stack depth (warp-uniform)
-    int nleaf_net = 0;   // leaves from the front
-    int nleaf_ins = 0;   // leaves from the back
+    // Keys-only / UNIQUE: the output is the unique order, so network leaves
+    // may run padded networks; they are kept in two lists (<= 8 items and
+    // 9..16) so each 32-leaf round runs the smallest network that fits.
+    // REF mode: one list, exact-size networks (DAG parity).
+    constexpr bool kPadAll = !std::is_same<typename Cfg::CX, CxRef>::value;
+    int sp = 0;          // stack depth (warp-uniform); entries 0..31 live in
+    uint32_t stk_reg = 0;  // lane registers (entry j in lane j), deeper ones in smem
+    int nleaf_net = 0;   // network leaves from the front (9..16 items when kPadAll)
+    int nleaf_small = 0; // kPadAll: network leaves of <= 8 items (second list)
+    int nleaf_ins = 0;   // insertion leaves from the back
     uint32_t state = prm.seed;
-    if (lane == 0) stk[0] = pack(0, n, 0, 0, 0);
-    sp = 1;
-    __syncwarp();
 
     auto add_leaf = [&](int lo, int cnt, int buf, int kind) {
       if (kind == LEAF_NET) {
-        if (lane == 0) leaf[nleaf_net] = pack(lo, cnt, 0, buf, LEAF_NET);
-        ++nleaf_net;
+        if (kPadAll && cnt <= 8) {
+          if (lane == 0) leaf[Cfg::NMAX_ + nleaf_small] = pack(lo, cnt, 0, buf, LEAF_NET);
+          ++nleaf_small;
+        } else {
+          if (lane == 0) leaf[nleaf_net] = pack(lo, cnt, 0, buf, LEAF_NET);
+          ++nleaf_net;
+        }
       } else {
         ++nleaf_ins;
         if (lane == 0) leaf[NMAX - nleaf_ins] = pack(lo, cnt, 0, buf, LEAF_INS);
@@ -244,38 +285,85 @@ __global__ void __launch_bounds__(RssCfg<U, P, NMAX, DAG, MODE, LAYOUT>::WARPS *
       else
         add_leaf(lo, cnt, buf, LEAF_INS);
     };
-
-    while (sp > 0) {
-      const uint32_t e = stk[sp - 1];
-      __syncwarp();
-      --sp;
-      const int lo = r_lo(e), cnt = r_cnt(e), depth = r_depth(e), buf = r_buf(e);
+    // The dispatch at the top of ns_rss_rec (netsort_core.c:325-345), applied
+    // when a range is CREATED: ranges that do not sample become leaves at once
+    // (they consume no draws, so the draw order is unchanged); only sampling
+    // ranges go through the stack.  Returns true if the range samples.
+    auto route = [&](int lo, int cnt, int depth, int buf) -> bool {
       if (cnt <= prm.threshold) {
         small_base(lo, cnt, buf);
-        continue;
+        return false;
       }
       if (cnt < sample) {
         if (cnt <= 16)
           small_base(lo, cnt, buf);
         else
           add_leaf(lo, cnt, buf, LEAF_INS);
-        continue;
+        return false;
       }
       if (depth >= 64 || sample > 64) {
         add_leaf(lo, cnt, buf, LEAF_INS);
-        continue;
+        return false;
+      }
+      return true;
+    };
+    auto push = [&](uint32_t e) {
+      if (sp < 32) {
+        if (lane == sp) stk_reg = e;
+      } else if (lane == 0) {
+        stk[sp - 32] = e;
+      }
+      ++sp;
+    };
+
+    // current sampling range; the first sampling child of a range is
+    // processed next without a stack round trip (its siblings are pushed so
+    // that the lowest bucket pops first: depth-first, bucket order)
+    int lo = 0, cnt = n, depth = 0, buf = 0;
+    bool have = route(0, n, 0, 0);
+    for (;;) {
+      if (!have) {
+        if (sp == 0) break;
+        --sp;
+        uint32_t e;
+        if (sp < 32) {
+          e = __shfl_sync(0xffffffffu, stk_reg, sp);
+        } else {
+          __syncwarp();
+          e = stk[sp - 32];
+          __syncwarp();
+        }
+        lo = r_lo(e);
+        cnt = r_cnt(e);
+        depth = r_depth(e);
+        buf = r_buf(e);
       }
       const U* kb = wb.keys(buf) + lo;
       // ---- sample: draws state^(t+1), t = 0..sample-1 ---------------------
       U* smp = wb.smp();
+      const uint32_t ucnt = uint32_t(cnt);
       U s_a = U(0), s_b = U(0);
-      const bool has_a = lane < sample, has_b = lane + 32 < sample;
-      if (has_a) s_a = kb[lcg_jump(state, lane + 1) % uint32_t(cnt)];
-      if (has_b) s_b = kb[lcg_jump(state, lane + 33) % uint32_t(cnt)];
+      if (lane < sample) s_a = kb[lcg_jump(state, lane + 1) % ucnt];
+      if (sample > 32) {
+        if (lane + 32 < sample) s_b = kb[lcg_jump(state, lane + 33) % ucnt];
+      }
       state = lcg_jump(state, sample);
       // rank among the sample (ties broken by draw index -> a total order)
       int ra = 0, rb = 0;
-      if (sample <= 32) {  // every config up to a = 8: one key per lane
+      if (sample <= 16) {  // a <= 4 (the paper's configs): two half-rankings
+        // lane g*16 + i ranks sample i against samples [g*h, g*h + h), h = sample/2;
+        // the raw samples are read back by broadcast from shared memory
+        U* raw = smp + 32;
+        if (lane < sample) raw[lane] = s_a;
+        __syncwarp();
+        const int i = lane & 15, h = sample >> 1, u0 = (lane >> 4) * h;
+        const U mine = raw[i];
+        for (int v = 0; v < h; ++v) {
+          const int u = u0 + v;
+          ra += lex_lt(raw[u], uint32_t(u), mine, uint32_t(i));
+        }
+        ra += __shfl_xor_sync(0xffffffffu, ra, 16);
+      } else if (sample <= 32) {  // one key per lane
         // (ku, u) < (s_a, lane) as one borrow chain; sample is a multiple of 4
 #pragma unroll 4
         for (int u = 0; u < sample; ++u) {
@@ -289,110 +377,136 @@ __global__ void __launch_bounds__(RssCfg<U, P, NMAX, DAG, MODE, LAYOUT>::WARPS *
           rb += (ku < s_b) || (ku == s_b && u < lane + 32);
         }
       }
-      if (has_a) smp[ra] = s_a;
-      if (has_b) smp[rb] = s_b;
+      if (sample > 16) __syncwarp();  // (the <= 16 path synchronised after its raw writes)
+      if (lane < sample) smp[ra] = s_a;
+      if (sample > 32 && lane + 32 < sample) smp[rb] = s_b;
       __syncwarp();
+      // (the next range's first shared-memory write is behind a __syncwarp
+      // that every lane reaches after these reads)
       const U s0 = smp[a - 1], s1 = smp[2 * a - 1], s2 = smp[3 * a - 1];
-      __syncwarp();
-      // ---- count -----------------------------------------------------------
-      int c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+      // ---- count: per-lane bucket counts packed two per word (16 bits) ----
+      uint32_t p01 = 0, p23 = 0;
       for (int i = lane; i < cnt; i += 32) {
         const U k = kb[i];
         const bool c = s1 < k;
         const U x = c ? s2 : s0;
-        const int tag = (int(c) << 1) + int(x < k);
-        c0 += tag == 0; c1 += tag == 1; c2 += tag == 2; c3 += tag == 3;
+        const uint32_t inc = x < k ? 0x10000u : 1u;
+        if (c) p23 += inc; else p01 += inc;
       }
-      c0 = __reduce_add_sync(0xffffffffu, c0);
-      c1 = __reduce_add_sync(0xffffffffu, c1);
-      c2 = __reduce_add_sync(0xffffffffu, c2);
-      c3 = __reduce_add_sync(0xffffffffu, c3);
+      p01 = __reduce_add_sync(0xffffffffu, p01);
+      p23 = __reduce_add_sync(0xffffffffu, p23);
+      const int c0 = int(p01 & 0xFFFFu), c1 = int(p01 >> 16), c2 = int(p23 & 0xFFFFu), c3 = int(p23 >> 16);
       const int big = max(max(c0, c1), max(c2, c3));
       if (big == cnt) {  // no progress possible: insertion sort (netsort_core.c:370-373)
         add_leaf(lo, cnt, buf, LEAF_INS);
+        have = false;
         continue;
       }
       // ---- stable scatter into the other buffer ---------------------------
+      // bucket = (c, d) = (s1 < k, (c ? s2 : s0) < k); running bucket
+      // offsets packed two per word like the counts
       const int ob = buf ^ 1;
       U* ko = wb.keys(ob) + lo;
       P* po = wb.pays(ob) + lo;
       const P* pb = wb.pays(buf) + lo;
-      int o0 = 0, o1 = c0, o2 = c0 + c1, o3 = c0 + c1 + c2;
+      uint32_t o01 = uint32_t(c0) << 16;
+      uint32_t o23 = uint32_t(c0 + c1) | (uint32_t(c0 + c1 + c2) << 16);
       for (int base = 0; base < cnt; base += 32) {
         const int i = base + lane;
         const bool live = i < cnt;
-        U k = U(0);
-        int tag = -1;
+        const unsigned lm = cnt - base >= 32 ? 0xffffffffu : ((1u << (cnt - base)) - 1u);
+        const U k = live ? kb[i] : U(0);
+        const bool c = s1 < k;
+        const U x = c ? s2 : s0;
+        const bool d = x < k;
+        const unsigned bc = __ballot_sync(0xffffffffu, c) & lm;
+        const unsigned bd = __ballot_sync(0xffffffffu, d) & lm;
+        const unsigned mm = (c ? bc : ~bc) & (d ? bd : ~bd) & lm;  // lanes of my bucket
+        const uint32_t w = c ? o23 : o01;
+        const int pos = int(d ? (w >> 16) : (w & 0xFFFFu)) + __popc(mm & lt_mask);
         if (live) {
-          k = kb[i];
-          const bool c = s1 < k;
-          const U x = c ? s2 : s0;
-          tag = (int(c) << 1) + int(x < k);
-        }
-        const unsigned m0 = __ballot_sync(0xffffffffu, tag == 0);
-        const unsigned m1 = __ballot_sync(0xffffffffu, tag == 1);
-        const unsigned m2 = __ballot_sync(0xffffffffu, tag == 2);
-        const unsigned m3 = __ballot_sync(0xffffffffu, tag == 3);
-        if (live) {
-          const unsigned mm = tag == 0 ? m0 : tag == 1 ? m1 : tag == 2 ? m2 : m3;
-          const int ob_ = tag == 0 ? o0 : tag == 1 ? o1 : tag == 2 ? o2 : o3;
-          const int pos = ob_ + __popc(mm & lt_mask);
           ko[pos] = k;
           if constexpr (Cfg::HAS_P) po[pos] = pb[i];
         }
-        o0 += __popc(m0); o1 += __popc(m1); o2 += __popc(m2); o3 += __popc(m3);
+        const uint32_t n11 = __popc(bc & bd), n10 = __popc(bc & ~bd), n01 = __popc(~bc & bd & lm);
+        const uint32_t n00 = uint32_t(__popc(lm)) - n11 - n10 - n01;
+        o01 += n00 | (n01 << 16);
+        o23 += n10 | (n11 << 16);
       }
       __syncwarp();
-      // ---- children, bucket 0 on top of the stack -------------------------
-      const int cs[4] = {c0, c1, c2, c3};
-      const int st[4] = {0, c0, c0 + c1, c0 + c1 + c2};
-#pragma unroll
-      for (int b = 3; b >= 0; --b) {
-        if (cs[b] > 1) {
-          if (lane == 0) stk[sp] = pack(lo + st[b], cs[b], depth + 1, ob, 0);
-          ++sp;
-        } else if (cs[b] == 1) {
-          add_leaf(lo + st[b], 1, ob, LEAF_NET);
+      // ---- children: route now; the lowest sampling bucket continues ------
+      int nlo = -1, ncnt = 0;  // pending sampling child (lowest bucket so far)
+      auto child = [&](int blo, int bcnt) {
+        if (bcnt > 0 && route(blo, bcnt, depth + 1, ob)) {
+          if (nlo >= 0) push(pack(nlo, ncnt, depth + 1, ob, 0));
+          nlo = blo;
+          ncnt = bcnt;
         }
+      };
+#pragma unroll 1
+      for (int b = 3; b >= 0; --b) {  // rolled: one copy of the routing code (I-cache)
+        const int bcnt = b == 3 ? c3 : b == 2 ? c2 : b == 1 ? c1 : c0;
+        const int boff = b == 3 ? c0 + c1 + c2 : b == 2 ? c0 + c1 : b == 1 ? c0 : 0;
+        child(lo + boff, bcnt);
       }
-      __syncwarp();
+      have = nlo >= 0;
+      if (have) {
+        lo = nlo;
+        cnt = ncnt;
+        depth += 1;
+        buf = ob;
+      }
     }
     __syncwarp();
 
     // ---- leaves: lane-parallel; results land in buffer A -------------------
-    for (int li = lane; li < nleaf_net; li += 32) {
-      const uint32_t e = leaf[li];
-      const int lo = r_lo(e), cnt = r_cnt(e), buf = r_buf(e);
-      const U* ks = wb.keys(buf) + lo;
-      const P* ps = wb.pays(buf) + lo;
-      // Keys-only / UNIQUE: every leaf runs the 16-channel network padded with
-      // +inf sentinels (output is the unique order; no per-size divergence).
-      // REF mode: exact-size networks, except 11..15 of the best family which
-      // ARE restrictions of Green's 16 (DAG-exact when padded).
-      constexpr bool kPadAll = !std::is_same<typename Cfg::CX, CxRef>::value;
-      const bool pad16 = kPadAll || (DAG == 0 && cnt >= 11);
-      E v[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        if (j < cnt) {
-          v[j].k = ks[j];
-          if constexpr (Cfg::HAS_P) v[j].p = ps[j];
-        } else {
-          v[j].k = U(~U(0));
-          if constexpr (Cfg::HAS_P) v[j].p = P(~P(0));
-        }
+    if constexpr (kPadAll) {
+      // rounds of 32 leaves; each round runs the smallest padded network that
+      // holds its longest leaf (+inf sentinels; the output is the unique order)
+      // rounds of 32 over [9..16-item leaves, then <= 8-item leaves]: a round
+      // whose longest leaf has <= 8 items runs the 8-channel network
+      const int nl = nleaf_net + nleaf_small;
+      for (int base = 0; base < nl; base += 32) {
+        const int li = base + lane;
+        const uint32_t e = li < nleaf_net ? leaf[li] : (li < nl ? leaf[Cfg::NMAX_ + li - nleaf_net] : 0u);
+        const int lo = r_lo(e), c = r_cnt(e), b = r_buf(e);
+        if (__reduce_max_sync(0xffffffffu, unsigned(c)) <= 8u)
+          leaf_pad<Cfg, DAG, 8>(wb, lo, c, b);
+        else
+          leaf_pad<Cfg, DAG, 16>(wb, lo, c, b);
       }
-      if (pad16)
-        Net<DAG, 16>::template run<typename Cfg::CX>(v);
-      else
-        leaf_network<Cfg, DAG>(v, cnt);
-      U* kd = wb.keys(0) + lo;
-      P* pd = wb.pays(0) + lo;
+    } else {
+      for (int li = lane; li < nleaf_net; li += 32) {
+        const uint32_t e = leaf[li];
+        const int lo = r_lo(e), cnt = r_cnt(e), buf = r_buf(e);
+        const U* ks = wb.keys(buf) + lo;
+        const P* ps = wb.pays(buf) + lo;
+        // REF mode: exact-size networks, except 11..15 of the best family
+        // which ARE restrictions of Green's 16 (DAG-exact when padded).
+        const bool pad16 = DAG == 0 && cnt >= 11;
+        E v[16];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        if (j < cnt) {
-          kd[j] = v[j].k;
-          if constexpr (Cfg::HAS_P) pd[j] = v[j].p;
+        for (int j = 0; j < 16; ++j) {
+          if (j < cnt) {
+            v[j].k = ks[j];
+            if constexpr (Cfg::HAS_P) v[j].p = ps[j];
+          } else {
+            v[j].k = U(~U(0));
+            if constexpr (Cfg::HAS_P) v[j].p = P(~P(0));
+          }
+        }
+        if (pad16)
+          Net<DAG, 16>::template run<typename Cfg::CX>(v);
+        else
+          leaf_network<Cfg, DAG>(v, cnt);
+        U* kd = wb.keys(0) + lo;
+        P* pd = wb.pays(0) + lo;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          if (j < cnt) {
+            kd[j] = v[j].k;
+            if constexpr (Cfg::HAS_P) pd[j] = v[j].p;
+          }
         }
       }
     }

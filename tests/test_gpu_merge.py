@@ -82,3 +82,32 @@ def test_cfg3_merge_full_size(n, torch):
     for name, x in (("uniform", uni), ("few16", few), ("sorted", srt), ("reverse", rev)):
         k, _ = batch.sort_rows(x, kind="merge")
         assert torch.equal(k, torch.sort(x, dim=1).values), name
+
+
+@pytest.mark.parametrize("n", [64, 128, 256, 512])
+@pytest.mark.parametrize("kdt", ["uint64", "int64", "uint32"])
+def test_merge_path_sentinel_ties(n, kdt, torch):
+    """Rows full of the largest key (the merge path's +inf sentinel value in
+    the ordered space -- all ones; INT64_MAX for signed keys ascending, the
+    minimum for descending) merge to the same values as np.sort: a lane whose
+    A run is exhausted may emit the sentinel for an equal B item."""
+    from paper_2002_05599_b200 import batch
+    rng = np.random.default_rng(n + 7)
+    info = np.iinfo(kdt)
+    rows = 999
+    choices = np.array([info.max, info.max - 1, info.min, 0, 5], dtype=kdt)
+    keys = choices[rng.integers(0, 5, size=(rows, n))]
+    keys[::3] = info.max
+    keys[1::3, : n // 2] = info.min
+    for desc in (False, True):
+        k, _ = batch.sort_rows(_t(torch, keys), kind="merge", descending=desc)
+        exp = np.sort(keys, axis=1)
+        if desc:
+            exp = exp[:, ::-1]
+        assert np.array_equal(k.cpu().numpy().view(keys.dtype), exp), (n, kdt, desc)
+    if kdt == "uint64":  # UNIQUE (key, payload) with all-ones payloads as well
+        pay = np.where(rng.integers(0, 2, size=(rows, n)) == 1, np.uint64(2**64 - 1), np.uint64(3))
+        for desc in (False, True):
+            ek, ep = oracle.typed_sort_rows(keys, pay, descending=desc, unique=True, kind="rss")
+            k, p = batch.sort_rows(_t(torch, keys), _t(torch, pay), kind="merge", descending=desc, tie="unique")
+            assert np.array_equal(k.cpu().numpy(), ek) and np.array_equal(p.cpu().numpy(), ep), (n, desc)

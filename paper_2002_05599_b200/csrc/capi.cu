@@ -111,9 +111,14 @@ int kernel_residency(const void* fn, int threads, int smem, int* ctas_per_sm, in
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+static int launch_direct(const KernelInfo& k, NetParams prm, cudaStream_t stream);
+static int64_t env_i64(const char* name, int64_t dflt);
+
 static int launch_net(const KernelInfo& k, NetParams prm, cudaStream_t stream) {
   if (!k.fn) return fail(NSG_ERR_SPEC, "no network kernel for this configuration");
   if (prm.rows <= 0) return 0;
+  static const int64_t direct_max = env_i64("NSG_DIRECT_MAX_MB", int64_t(1) << 40) << 20;
+  if (k.direct_fn && prm.rows * k.row_bytes <= direct_max) return launch_direct(k, prm, stream);
   LaunchGeom g;
   if (int rc = launch_geom(k.fn, k.threads, k.smem, &g)) return rc;
   const int64_t tiles = (prm.rows + k.rows_per_warp - 1) / k.rows_per_warp;
@@ -121,6 +126,27 @@ static int launch_net(const KernelInfo& k, NetParams prm, cudaStream_t stream) {
   const int64_t grid = std::min<int64_t>(ctas_needed, int64_t(g.sms) * g.ctas_per_sm);
   void* args[] = {&prm};
   NSG_CUDA(cudaLaunchKernel(k.fn, dim3(unsigned(grid)), dim3(unsigned(k.threads)), args, size_t(k.smem), stream));
+  return 0;
+}
+
+static int64_t env_i64(const char* name, int64_t dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoll(e) : dflt;
+}
+
+// Shapes with a register-direct kernel (net_direct_kernel: rows of <= 16,
+// 24 or 16k bytes) use it at every batch size; NSG_DIRECT_MAX_MB caps the
+// batch (0 = always the pipelined kernel; A/B measurements only).  One CTA
+// of 256 threads per ~NSG_DIRECT_CTA_KB (8) KiB of rows, grid-stride beyond
+// the 2^30 CTA limit: the CTA scheduler streams CTAs in as others retire.
+static int launch_direct(const KernelInfo& k, NetParams prm, cudaStream_t stream) {
+  static const int64_t cta_bytes = env_i64("NSG_DIRECT_CTA_KB", 8) << 10;
+  const int64_t rows_per_cta = std::max<int64_t>(256, cta_bytes / k.row_bytes / 256 * 256);
+  const int64_t grid = std::min<int64_t>((prm.rows + rows_per_cta - 1) / rows_per_cta, int64_t(1) << 30);
+  LaunchGeom g;
+  if (int rc = launch_geom(k.direct_fn, 256, 0, &g)) return rc;
+  void* args[] = {&prm};
+  NSG_CUDA(cudaLaunchKernel(k.direct_fn, dim3(unsigned(grid)), dim3(256), args, 0, stream));
   return 0;
 }
 

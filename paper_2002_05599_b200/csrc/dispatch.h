@@ -11,6 +11,8 @@ struct KernelInfo {
   int threads = 0;           // threads per CTA
   int rows_per_warp = 0;     // rows in one warp tile
   int warps = 0;             // warps per CTA
+  int row_bytes = 0;         // key + payload bytes of one (sub-)row
+  const void* direct_fn = nullptr;  // register-direct kernel for this shape (net_direct_kernel), or null
 };
 
 // key_bytes 4/8; pay 0 none / 1 u32 / 2 u64; mode 0 REF / 1 UNIQUE; layout 0 SoA / 1 AoS16

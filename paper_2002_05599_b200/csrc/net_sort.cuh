@@ -632,4 +632,93 @@ __global__ void __launch_bounds__(Cfg::WARPS * 32, 1) net_sort_kernel(const NetP
   cp_async_wait<0>();
 }
 
+// ---- register-direct path --------------------------------------------------
+// Rows whose key (and payload) row is <= 16, 24, 32, 48 or 64 bytes: each thread loads its row straight from HBM with vector loads (a
+// warp's 32 consecutive rows are one contiguous span, so every DRAM sector is
+// read once; the L1 serves the other vectors of a row), sorts in registers
+// and writes back with vector streaming stores -- no shared memory and no
+// per-warp pipeline.  Measured faster than the pipelined kernel above for
+// these shapes at every batch size (BASELINE cfg1: 18.4 -> 14.3 us, equal to
+// a plain 32 MiB device copy; 2^24-row cfg2 cells 5-20 % faster, DESIGN.md
+// §3.1); rows of 40, 56, 72.. bytes keep the pipelined kernel (their
+// misaligned 8-byte vectors make the direct loads L1-bound).
+// (rows above 64 bytes lose: a warp's 32 rows then span 32+ L1 lines per
+// vector load and the lines are evicted before the row's other vectors are
+// read -- 128-byte rows measured 3.9 vs 6.2-6.5 TB/s pipelined)
+__host__ __device__ constexpr bool direct_row_ok(int r) { return r <= 16 || r == 24 || (r % 16 == 0 && r <= 64); }
+
+template <class Cfg>
+struct DirectOk {
+  static constexpr bool value = Cfg::G == 1 && Cfg::N >= 2 && direct_row_ok(Cfg::GK::R) &&
+                                (Cfg::PEB == 0 || direct_row_ok(Cfg::GP::R));
+};
+
+template <class G>
+__device__ __forceinline__ void ldg_row(const unsigned char* g, uint32_t (&w)[G::W]) {
+#pragma unroll
+  for (int i = 0; i < G::R / G::V; ++i) {
+    if constexpr (G::V == 16) {
+      const uint4 x = *reinterpret_cast<const uint4*>(g + 16 * i);
+      w[4 * i] = x.x; w[4 * i + 1] = x.y; w[4 * i + 2] = x.z; w[4 * i + 3] = x.w;
+    } else if constexpr (G::V == 8) {
+      const uint2 x = *reinterpret_cast<const uint2*>(g + 8 * i);
+      w[2 * i] = x.x; w[2 * i + 1] = x.y;
+    } else {
+      w[i] = *reinterpret_cast<const uint32_t*>(g + 4 * i);
+    }
+  }
+}
+
+template <class Cfg>
+__global__ void __launch_bounds__(256) net_direct_kernel(const NetParams p) {
+  using U = typename Cfg::U;
+  using P = typename Cfg::P;
+  using GK = typename Cfg::GK;
+  using GP = typename Cfg::GP;
+  constexpr int N = Cfg::N;
+  const unsigned char* kin = static_cast<const unsigned char*>(p.k_in);
+  const unsigned char* pin = static_cast<const unsigned char*>(p.p_in);
+  unsigned char* kout = static_cast<unsigned char*>(p.k_out);
+  unsigned char* pout = static_cast<unsigned char*>(p.p_out);
+  const int64_t nthreads = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t row = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; row < p.rows; row += nthreads) {
+    uint32_t wk[GK::W];
+    uint32_t wp[Cfg::PEB ? GP::W : 1];
+    ldg_row<GK>(kin + row * GK::R, wk);
+    if constexpr (Cfg::PEB != 0) ldg_row<GP>(pin + row * GP::R, reinterpret_cast<uint32_t(&)[GP::W]>(wp));
+    Elem<U, P> e[N];
+    if constexpr (Cfg::LAYOUT == LAYOUT_AOS16) {
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        e[j].k = word_get<uint64_t>(wk, 2 * j);
+        e[j].p = word_get<uint64_t>(wk, 2 * j + 1);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < N; ++j) e[j].k = word_get<U>(wk, j);
+      if constexpr (Cfg::HAS_P) {
+#pragma unroll
+        for (int j = 0; j < N; ++j) e[j].p = word_get<P>(wp, j);
+      }
+    }
+    sort_elems<Cfg>(e, p.xf);
+    if constexpr (Cfg::LAYOUT == LAYOUT_AOS16) {
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        word_put(wk, 2 * j, e[j].k);
+        word_put(wk, 2 * j + 1, e[j].p);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < N; ++j) word_put(wk, j, e[j].k);
+      if constexpr (Cfg::HAS_P) {
+#pragma unroll
+        for (int j = 0; j < N; ++j) word_put(wp, j, e[j].p);
+      }
+    }
+    stg_row<GK>(kout + row * GK::R, wk);
+    if constexpr (Cfg::PEB != 0) stg_row<GP>(pout + row * GP::R, reinterpret_cast<const uint32_t(&)[GP::W]>(wp));
+  }
+}
+
 }  // namespace nsg

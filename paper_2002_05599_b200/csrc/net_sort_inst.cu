@@ -21,6 +21,8 @@ KernelInfo info() {
   k.threads = C::WARPS * 32;
   k.rows_per_warp = C::ROWS;
   k.warps = C::WARPS;
+  k.row_bytes = C::ROW_BYTES;
+  if constexpr (DirectOk<C>::value) k.direct_fn = reinterpret_cast<const void*>(&net_direct_kernel<C>);
   return k;
 }
 

@@ -642,10 +642,16 @@ __global__ void __launch_bounds__(Cfg::WARPS * 32, 1) net_sort_kernel(const NetP
 // a plain 32 MiB device copy; 2^24-row cfg2 cells 5-20 % faster, DESIGN.md
 // §3.1); rows of 40, 56, 72.. bytes keep the pipelined kernel (their
 // misaligned 8-byte vectors make the direct loads L1-bound).
-// (rows above 64 bytes lose: a warp's 32 rows then span 32+ L1 lines per
-// vector load and the lines are evicted before the row's other vectors are
-// read -- 128-byte rows measured 3.9 vs 6.2-6.5 TB/s pipelined)
-__host__ __device__ constexpr bool direct_row_ok(int r) { return r <= 16 || r == 24 || (r % 16 == 0 && r <= 64); }
+// (rows above 64 bytes lose: every 16-byte vector load of a warp then touches
+// 32 different 128-byte L1 lines, and at 16 bytes per line access the L1 tag
+// rate caps the kernel near 4.5 TB/s -- 128-byte rows measured 3.9-4.7 TB/s
+// direct against 6.0-6.6 pipelined, with or without an occupancy cap)
+#ifndef NSG_DIRECT_MAX_ROW
+#define NSG_DIRECT_MAX_ROW 64
+#endif
+__host__ __device__ constexpr bool direct_row_ok(int r) {
+  return r <= 16 || r == 24 || (r % 16 == 0 && r <= NSG_DIRECT_MAX_ROW);
+}
 
 template <class Cfg>
 struct DirectOk {

@@ -78,7 +78,12 @@ class Cell:
     def kernel_key(self) -> str:  # name used by tools/profile_summary.py / profiles/traffic.json
         fam = "best" if self.family == "best" else "bn"
         pay = {0: "keys", 4: "p32", 8: "p64"}[self.pb]
-        return f"net_sort n={self.n} {fam} {'u64' if self.kb == 8 else 'u32'} {pay} SoA UNIQUE"
+        # rows of <= 64 bytes per region run the register-direct kernel
+        # (net_direct_kernel, csrc/net_sort.cuh direct_row_ok)
+        ok = lambda r: r <= 16 or r == 24 or (r % 16 == 0 and r <= 64)  # noqa: E731
+        direct = ok(self.n * self.kb) and (self.pb == 0 or ok(self.n * self.pb))
+        kind = "net_direct" if direct else "net_sort"
+        return f"{kind} n={self.n} {fam} {'u64' if self.kb == 8 else 'u32'} {pay} SoA UNIQUE"
 
 
 def make_cells(args, rows):

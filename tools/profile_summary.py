@@ -52,7 +52,8 @@ def short_name(name: str) -> str:
         fam = {"0": "best", "1": "bn", "2": "merge"}[dag]
         kt = "u64" if "long" in u else "u32"
         pt = {"NoPay": "keys", "unsigned int": "p32", "unsigned long": "p64"}.get(p.strip(), p)
-        return f"net_sort n={n} {fam} {kt} {pt} {'AoS' if lay == '1' else 'SoA'} {'UNIQUE' if mode == '1' else 'REF'}"
+        kind = "net_direct" if "net_direct_kernel" in name else "net_sort"
+        return f"{kind} n={n} {fam} {kt} {pt} {'AoS' if lay == '1' else 'SoA'} {'UNIQUE' if mode == '1' else 'REF'}"
     return name[:90]
 
 

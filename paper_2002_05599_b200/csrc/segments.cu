@@ -157,24 +157,47 @@ __device__ __forceinline__ void store_range(const unsigned char* sm, T* dst, uin
   }
 }
 
-// One segment of exactly L items (already in the ordered key space): load,
-// network, store.  The length is a template constant, so each switch case
-// touches exactly L slots and stays small (the order transform runs once per
-// element in the staging passes instead).
-template <int L, class U, class P, int DAG, class CX>
-__device__ __forceinline__ void sort_segment_len(U* keys, P* pays) {
+// Order transform kinds (template XK): none, generic, float descending.  The
+// transform is applied in registers around each network and nowhere else:
+// elements of single-item segments are staged and stored untouched, which is
+// exactly what the transform pair would produce (it is a bijection and its
+// inverse), so no staging pass has to visit every element.
+enum { XK_NONE = 0, XK_GEN = 1, XK_FDESC = 2 };
+template <int XK, class U>
+__device__ __forceinline__ U xk_to(U k, const Xform& xf) {
+  if constexpr (XK == XK_GEN) return to_ord<U>(k, xf);
+  else if constexpr (XK == XK_FDESC) return fdesc_ord<U>(k);
+  else return k;
+}
+template <int XK, class U>
+__device__ __forceinline__ U xk_from(U k, const Xform& xf) {
+  if constexpr (XK == XK_GEN) return from_ord<U>(k, xf);
+  else if constexpr (XK == XK_FDESC) return fdesc_ord<U>(k);
+  else return k;
+}
+template <int XK, class P>
+__device__ __forceinline__ P xk_pay(P q, const Xform& xf) {
+  if constexpr (XK == XK_NONE) return q;
+  else return P(q ^ P(xf.pdesc));
+}
+
+// One segment of exactly L items: load (into the ordered space), network,
+// store.  The length is a template constant, so each switch case touches
+// exactly L slots and stays small.
+template <int L, class U, class P, int DAG, class CX, int XK>
+__device__ __forceinline__ void sort_segment_len(U* keys, P* pays, const Xform& xf) {
   constexpr bool HAS_P = !IsNoPay<P>::value;
   Elem<U, P> v[L];
 #pragma unroll
   for (int j = 0; j < L; ++j) {
-    v[j].k = keys[j];
-    if constexpr (HAS_P) v[j].p = pays[j];
+    v[j].k = xk_to<XK>(keys[j], xf);
+    if constexpr (HAS_P) v[j].p = xk_pay<XK>(pays[j], xf);
   }
   Net<DAG, L>::template run<CX>(v);
 #pragma unroll
   for (int j = 0; j < L; ++j) {
-    keys[j] = v[j].k;
-    if constexpr (HAS_P) pays[j] = v[j].p;
+    keys[j] = xk_from<XK>(v[j].k, xf);
+    if constexpr (HAS_P) pays[j] = xk_pay<XK>(v[j].p, xf);
   }
 }
 
@@ -185,15 +208,15 @@ __device__ __forceinline__ void sort_segment_len(U* keys, P* pays) {
 // it is DAG-exact even in REF mode; for any family it is exact in UNIQUE /
 // keys-only mode.  One code path for the long lengths keeps the warps of a
 // mixed-length chunk converged and the kernel's instruction footprint small.
-template <class U, class P, int DAG, class CX>
-__device__ __forceinline__ void sort_segment_pad16(U* keys, P* pays, int len) {
+template <class U, class P, int DAG, class CX, int XK>
+__device__ __forceinline__ void sort_segment_pad16(U* keys, P* pays, int len, const Xform& xf) {
   constexpr bool HAS_P = !IsNoPay<P>::value;
   Elem<U, P> v[16];
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
     if (j < 11 || j < len) {
-      v[j].k = keys[j];
-      if constexpr (HAS_P) v[j].p = pays[j];
+      v[j].k = xk_to<XK>(keys[j], xf);
+      if constexpr (HAS_P) v[j].p = xk_pay<XK>(pays[j], xf);
     } else {
       v[j].k = U(~U(0));
       if constexpr (HAS_P) v[j].p = P(~P(0));
@@ -203,40 +226,40 @@ __device__ __forceinline__ void sort_segment_pad16(U* keys, P* pays, int len) {
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
     if (j < 11 || j < len) {
-      keys[j] = v[j].k;
-      if constexpr (HAS_P) pays[j] = v[j].p;
+      keys[j] = xk_from<XK>(v[j].k, xf);
+      if constexpr (HAS_P) pays[j] = xk_pay<XK>(v[j].p, xf);
     }
   }
 }
 
-template <class U, class P, int DAG, class CX>
-__device__ __forceinline__ void sort_segment_smem(U* keys, P* pays, int len) {
+template <class U, class P, int DAG, class CX, int XK>
+__device__ __forceinline__ void sort_segment_smem(U* keys, P* pays, int len, const Xform& xf) {
   constexpr bool kPad16 = DAG == 0 || !std::is_same<CX, CxRef>::value;
   if constexpr (kPad16) {
     if (len >= 11) {
-      sort_segment_pad16<U, P, DAG, CX>(keys, pays, len);
+      sort_segment_pad16<U, P, DAG, CX, XK>(keys, pays, len, xf);
       return;
     }
   }
   switch (kPad16 ? (len > 10 ? 0 : len) : len) {
-    case 2: sort_segment_len<2, U, P, DAG, CX>(keys, pays); break;
-    case 3: sort_segment_len<3, U, P, DAG, CX>(keys, pays); break;
-    case 4: sort_segment_len<4, U, P, DAG, CX>(keys, pays); break;
-    case 5: sort_segment_len<5, U, P, DAG, CX>(keys, pays); break;
-    case 6: sort_segment_len<6, U, P, DAG, CX>(keys, pays); break;
-    case 7: sort_segment_len<7, U, P, DAG, CX>(keys, pays); break;
-    case 8: sort_segment_len<8, U, P, DAG, CX>(keys, pays); break;
-    case 9: sort_segment_len<9, U, P, DAG, CX>(keys, pays); break;
-    case 10: sort_segment_len<10, U, P, DAG, CX>(keys, pays); break;
+    case 2: sort_segment_len<2, U, P, DAG, CX, XK>(keys, pays, xf); break;
+    case 3: sort_segment_len<3, U, P, DAG, CX, XK>(keys, pays, xf); break;
+    case 4: sort_segment_len<4, U, P, DAG, CX, XK>(keys, pays, xf); break;
+    case 5: sort_segment_len<5, U, P, DAG, CX, XK>(keys, pays, xf); break;
+    case 6: sort_segment_len<6, U, P, DAG, CX, XK>(keys, pays, xf); break;
+    case 7: sort_segment_len<7, U, P, DAG, CX, XK>(keys, pays, xf); break;
+    case 8: sort_segment_len<8, U, P, DAG, CX, XK>(keys, pays, xf); break;
+    case 9: sort_segment_len<9, U, P, DAG, CX, XK>(keys, pays, xf); break;
+    case 10: sort_segment_len<10, U, P, DAG, CX, XK>(keys, pays, xf); break;
     default:
       if constexpr (!kPad16) {
         switch (len) {
-          case 11: sort_segment_len<11, U, P, DAG, CX>(keys, pays); break;
-          case 12: sort_segment_len<12, U, P, DAG, CX>(keys, pays); break;
-          case 13: sort_segment_len<13, U, P, DAG, CX>(keys, pays); break;
-          case 14: sort_segment_len<14, U, P, DAG, CX>(keys, pays); break;
-          case 15: sort_segment_len<15, U, P, DAG, CX>(keys, pays); break;
-          case 16: sort_segment_len<16, U, P, DAG, CX>(keys, pays); break;
+          case 11: sort_segment_len<11, U, P, DAG, CX, XK>(keys, pays, xf); break;
+          case 12: sort_segment_len<12, U, P, DAG, CX, XK>(keys, pays, xf); break;
+          case 13: sort_segment_len<13, U, P, DAG, CX, XK>(keys, pays, xf); break;
+          case 14: sort_segment_len<14, U, P, DAG, CX, XK>(keys, pays, xf); break;
+          case 15: sort_segment_len<15, U, P, DAG, CX, XK>(keys, pays, xf); break;
+          case 16: sort_segment_len<16, U, P, DAG, CX, XK>(keys, pays, xf); break;
           default: break;
         }
       }
@@ -244,7 +267,7 @@ __device__ __forceinline__ void sort_segment_smem(U* keys, P* pays, int len) {
   }
 }
 
-template <class U, class P, int MODE, int DAG>
+template <class U, class P, int MODE, int DAG, int XK>
 __global__ void __launch_bounds__(kThreads, NSG_SEG_MINB) seg_kernel(const SegParams prm) {
   using G = SegGeom<U, P>;
   constexpr bool HAS_P = !IsNoPay<P>::value;
@@ -297,38 +320,6 @@ __global__ void __launch_bounds__(kThreads, NSG_SEG_MINB) seg_kernel(const SegPa
     unsigned char* kb = buf + range_shift<int(sizeof(U))>(e0);
     unsigned char* pb = buf + G::K_REG + (HAS_P ? range_shift<G::PB>(e0) : 0);
     // hist[] is zero here (prologue / previous call); callers synchronise first
-    if (staged && xf.active) {  // into the ordered key space, once per element,
-      // 16 bytes at a time over the whole staged chunk range (edge elements of
-      // the neighbouring tiles are transformed too, but never stored)
-      const int kchunks = int((uint64_t(e1) * sizeof(U) + 15) / 16 - (uint64_t(e0) * sizeof(U)) / 16);
-      const bool fd = is_fdesc(xf);
-      for (int c = tid; c < kchunks; c += kThreads) {
-        union {
-          uint4 v;
-          U e[16 / sizeof(U)];
-        } u;
-        u.v = reinterpret_cast<uint4*>(buf)[c];
-        if (fd) {
-#pragma unroll
-          for (int i = 0; i < int(16 / sizeof(U)); ++i) u.e[i] = fdesc_ord<U>(u.e[i]);
-        } else {
-#pragma unroll
-          for (int i = 0; i < int(16 / sizeof(U)); ++i) u.e[i] = to_ord<U>(u.e[i], xf);
-        }
-        reinterpret_cast<uint4*>(buf)[c] = u.v;
-      }
-      if constexpr (HAS_P) {
-        if (xf.pdesc) {
-          const int pchunks = int((uint64_t(e1) * G::PB + 15) / 16 - (uint64_t(e0) * G::PB) / 16);
-          uint4* pc = reinterpret_cast<uint4*>(buf + G::K_REG);
-          for (int c = tid; c < pchunks; c += kThreads) {
-            uint4 x = pc[c];
-            x.x = ~x.x; x.y = ~x.y; x.z = ~x.z; x.w = ~x.w;
-            pc[c] = x;
-          }
-        }
-      }
-    }
     // each thread bins its SPT segments; the rank atomicAdd returns inside a
     // length bin is kept in registers and placed after the scan
     constexpr int SPT = (TS_ + kThreads - 1) / kThreads;
@@ -385,24 +376,16 @@ __global__ void __launch_bounds__(kThreads, NSG_SEG_MINB) seg_kernel(const SegPa
         if (j < nshort) {
           const int s = a + perm[j];
           const int st = int(offs[s] - e0);
-          sort_segment_smem<U, P, DAG, CX>(reinterpret_cast<U*>(kb) + st, reinterpret_cast<P*>(pb) + st,
-                                           int(offs[s + 1] - offs[s]));
+          sort_segment_smem<U, P, DAG, CX, XK>(reinterpret_cast<U*>(kb) + st, reinterpret_cast<P*>(pb) + st,
+                                               int(offs[s + 1] - offs[s]), xf);
         }
       }
     }
     __syncthreads();
     if (tid < 32) hist[tid] = 0;  // ready for the next call (after its leading sync)
-    if (staged) {
-      if (xf.active) {
-        if (is_fdesc(xf))
-          store_range<U>(buf, kout, e0, e1, tid, [](U k) { return fdesc_ord<U>(k); });
-        else
-          store_range<U>(buf, kout, e0, e1, tid, [&](U k) { return from_ord<U>(k, xf); });
-        if constexpr (HAS_P) store_range<P>(buf + G::K_REG, pout, e0, e1, tid, [&](P q) { return P(q ^ P(xf.pdesc)); });
-      } else {
-        store_range<U>(buf, kout, e0, e1, tid, [](U k) { return k; });
-        if constexpr (HAS_P) store_range<P>(buf + G::K_REG, pout, e0, e1, tid, [](P q) { return q; });
-      }
+    if (staged) {  // (elements are back in their own representation)
+      store_range<U>(buf, kout, e0, e1, tid, [](U k) { return k; });
+      if constexpr (HAS_P) store_range<P>(buf + G::K_REG, pout, e0, e1, tid, [](P q) { return q; });
     }
     // no trailing barrier: the next tile starts with wait + __syncthreads
   };
@@ -477,21 +460,27 @@ struct SegKernel {
   int ts;
 };
 
+template <class U, class P, int MODE, int DAG, int XK>
+SegKernel seg_info_xk() {
+  return {reinterpret_cast<const void*>(&seg_kernel<U, P, MODE, DAG, XK>), SegGeom<U, P>::SMEM, SegGeom<U, P>::TS};
+}
 template <class U, class P, int MODE, int DAG>
-SegKernel seg_info() {
-  return {reinterpret_cast<const void*>(&seg_kernel<U, P, MODE, DAG>), SegGeom<U, P>::SMEM, SegGeom<U, P>::TS};
+SegKernel seg_info(int xk) {
+  if (xk == XK_FDESC) return seg_info_xk<U, P, MODE, DAG, XK_FDESC>();
+  if (xk == XK_GEN) return seg_info_xk<U, P, MODE, DAG, XK_GEN>();
+  return seg_info_xk<U, P, MODE, DAG, XK_NONE>();
 }
 
 template <int DAG>
-SegKernel seg_pick_dag(int kb, int pay, int mode) {
+SegKernel seg_pick_dag(int kb, int pay, int mode, int xk) {
   if (kb == 4) {
-    if (pay == 0) return seg_info<uint32_t, NoPay, MODE_UNIQUE, DAG>();
-    if (pay == 1) return mode ? seg_info<uint32_t, uint32_t, MODE_UNIQUE, DAG>() : seg_info<uint32_t, uint32_t, MODE_REF, DAG>();
-    return mode ? seg_info<uint32_t, uint64_t, MODE_UNIQUE, DAG>() : seg_info<uint32_t, uint64_t, MODE_REF, DAG>();
+    if (pay == 0) return seg_info<uint32_t, NoPay, MODE_UNIQUE, DAG>(xk);
+    if (pay == 1) return mode ? seg_info<uint32_t, uint32_t, MODE_UNIQUE, DAG>(xk) : seg_info<uint32_t, uint32_t, MODE_REF, DAG>(xk);
+    return mode ? seg_info<uint32_t, uint64_t, MODE_UNIQUE, DAG>(xk) : seg_info<uint32_t, uint64_t, MODE_REF, DAG>(xk);
   }
-  if (pay == 0) return seg_info<uint64_t, NoPay, MODE_UNIQUE, DAG>();
-  if (pay == 1) return mode ? seg_info<uint64_t, uint32_t, MODE_UNIQUE, DAG>() : seg_info<uint64_t, uint32_t, MODE_REF, DAG>();
-  return mode ? seg_info<uint64_t, uint64_t, MODE_UNIQUE, DAG>() : seg_info<uint64_t, uint64_t, MODE_REF, DAG>();
+  if (pay == 0) return seg_info<uint64_t, NoPay, MODE_UNIQUE, DAG>(xk);
+  if (pay == 1) return mode ? seg_info<uint64_t, uint32_t, MODE_UNIQUE, DAG>(xk) : seg_info<uint64_t, uint32_t, MODE_REF, DAG>(xk);
+  return mode ? seg_info<uint64_t, uint64_t, MODE_UNIQUE, DAG>(xk) : seg_info<uint64_t, uint64_t, MODE_REF, DAG>(xk);
 }
 
 int key_bytes_of(int dt) { return (dt == NSG_KEY_U32 || dt == NSG_KEY_I32 || dt == NSG_KEY_F32) ? 4 : 8; }
@@ -514,9 +503,11 @@ int launch_segments(const nsg_spec& sp, const uint32_t* offsets, int64_t nseg, c
   if (e != cudaSuccess) return fail(NSG_ERR_CUDA, "memset: %s", cudaGetErrorString(e));
   const int kb = key_bytes_of(sp.key_dtype);
   const int dag = sp.family == 0 ? 0 : 1;
-  const SegKernel k = dag ? seg_pick_dag<1>(kb, sp.payload_dtype, sp.tie_mode)
-                          : seg_pick_dag<0>(kb, sp.payload_dtype, sp.tie_mode);
-  SegParams prm{offsets, nseg, keys_in, keys_out, pay_in, pay_out, make_xform(sp), w, w + 4, cap, w + 1};
+  const Xform xf = make_xform(sp);
+  const int xk = !xf.active ? XK_NONE : ((xf.flt && xf.kdesc) ? XK_FDESC : XK_GEN);
+  const SegKernel k = dag ? seg_pick_dag<1>(kb, sp.payload_dtype, sp.tie_mode, xk)
+                          : seg_pick_dag<0>(kb, sp.payload_dtype, sp.tie_mode, xk);
+  SegParams prm{offsets, nseg, keys_in, keys_out, pay_in, pay_out, xf, w, w + 4, cap, w + 1};
   int sms = 0, occ = 0;
   if (int rc = kernel_residency(k.fn, kThreads, k.smem, &occ, &sms)) return rc;
   const int64_t ntiles = (nseg + k.ts - 1) / k.ts;

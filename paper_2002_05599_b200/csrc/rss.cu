@@ -87,7 +87,6 @@ __device__ __forceinline__ int r_lo(uint32_t e) { return int(e & 2047u); }
 __device__ __forceinline__ int r_cnt(uint32_t e) { return int((e >> 11) & 2047u); }
 __device__ __forceinline__ int r_depth(uint32_t e) { return int((e >> 22) & 127u); }
 __device__ __forceinline__ int r_buf(uint32_t e) { return int((e >> 29) & 1u); }
-__device__ __forceinline__ int r_kind(uint32_t e) { return int(e >> 30); }
 
 enum LeafKind { LEAF_NET = 0, LEAF_INS = 1 };
 
@@ -434,25 +433,67 @@ __global__ void __launch_bounds__(RssCfg<U, P, NMAX, DAG, MODE, LAYOUT>::WARPS *
         o23 += n10 | (n11 << 16);
       }
       __syncwarp();
-      // ---- children: route now; the lowest sampling bucket continues ------
-      int nlo = -1, ncnt = 0;  // pending sampling child (lowest bucket so far)
-      auto child = [&](int blo, int bcnt) {
-        if (bcnt > 0 && route(blo, bcnt, depth + 1, ob)) {
-          if (nlo >= 0) push(pack(nlo, ncnt, depth + 1, ob, 0));
-          nlo = blo;
-          ncnt = bcnt;
-        }
-      };
-#pragma unroll 1
-      for (int b = 3; b >= 0; --b) {  // rolled: one copy of the routing code (I-cache)
-        const int bcnt = b == 3 ? c3 : b == 2 ? c2 : b == 1 ? c1 : c0;
-        const int boff = b == 3 ? c0 + c1 + c2 : b == 2 ? c0 + c1 : b == 1 ? c0 : 0;
-        child(lo + boff, bcnt);
+      // ---- children, routed lane-parallel: lane b < 4 routes bucket b ------
+      // (the dispatch of `route` above, per lane); leaves are appended with
+      // ballot ranks, sampling buckets other than the lowest are pushed
+      // highest first, and the lowest sampling bucket continues directly.
+      enum { K_NONE = 0, K_NET = 1, K_NETS = 2, K_INS = 3, K_SMP = 4 };
+      int bcnt = 0, boff = 0;
+      if (lane < 4) {
+        bcnt = lane == 3 ? c3 : lane == 2 ? c2 : lane == 1 ? c1 : c0;
+        boff = lane == 3 ? c0 + c1 + c2 : lane == 2 ? c0 + c1 : lane == 1 ? c0 : 0;
       }
-      have = nlo >= 0;
+      int kind = K_NONE;
+      if (bcnt == 1) {
+        kind = K_NET;
+      } else if (bcnt >= 2) {
+        const bool base_net = prm.base_kind == 0 && bcnt <= 16;  // ns_small_base
+        if (bcnt <= prm.threshold || bcnt < sample)
+          kind = base_net ? K_NET : K_INS;
+        else if (depth + 1 >= 64 || sample > 64)
+          kind = K_INS;
+        else
+          kind = K_SMP;
+      }
+      if (kPadAll && kind == K_NET && bcnt <= 8) kind = K_NETS;
+      const uint32_t ent = pack(lo + boff, bcnt, depth + 1, ob, kind == K_INS ? LEAF_INS : 0);
+      const unsigned m_net = __ballot_sync(0xffffffffu, kind == K_NET);
+      const unsigned m_nets = __ballot_sync(0xffffffffu, kind == K_NETS);
+      const unsigned m_ins = __ballot_sync(0xffffffffu, kind == K_INS);
+      const unsigned m_smp = __ballot_sync(0xffffffffu, kind == K_SMP);
+      if (kind == K_NET) leaf[nleaf_net + __popc(m_net & lt_mask)] = ent;
+      if (kind == K_NETS) leaf[Cfg::NMAX_ + nleaf_small + __popc(m_nets & lt_mask)] = ent;
+      if (kind == K_INS) leaf[NMAX - 1 - (nleaf_ins + __popc(m_ins & lt_mask))] = ent;
+      nleaf_net += __popc(m_net);
+      nleaf_small += __popc(m_nets);
+      nleaf_ins += __popc(m_ins);
+      have = m_smp != 0;
       if (have) {
-        lo = nlo;
-        cnt = ncnt;
+        const int first = __ffs(m_smp) - 1;
+        const unsigned m_push = m_smp & (m_smp - 1);  // all but the lowest
+        const int npush = __popc(m_push);
+        if (npush) {
+          if (sp + npush <= 32) {
+            // slot sp + k takes the k-th highest pushed bucket
+            const int k = lane - sp;
+            const unsigned q1 = m_push & ~(0x80000000u >> __clz(m_push));  // (npush <= 3)
+            const int h0 = 31 - __clz(m_push), h1 = q1 ? 31 - __clz(q1) : 0;
+            const unsigned q2 = q1 & ~(q1 ? 0x80000000u >> __clz(q1) : 0u);
+            const int h2 = q2 ? 31 - __clz(q2) : 0;
+            const int src = k == 0 ? h0 : k == 1 ? h1 : h2;
+            const uint32_t v = __shfl_sync(0xffffffffu, ent, src);
+            if (k >= 0 && k < npush) stk_reg = v;
+            sp += npush;
+          } else {  // (deep stacks: entry by entry, spilling to shared memory)
+            for (int bb = 3; bb > first; --bb) {
+              const uint32_t v = __shfl_sync(0xffffffffu, ent, bb);
+              if ((m_push >> bb) & 1u) push(v);
+            }
+          }
+        }
+        const uint32_t e = __shfl_sync(0xffffffffu, ent, first);
+        lo = r_lo(e);
+        cnt = r_cnt(e);
         depth += 1;
         buf = ob;
       }

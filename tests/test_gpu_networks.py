@@ -283,3 +283,61 @@ def test_cfg5_shard_properties(torch):
     assert torch.equal(p.view(torch.int64)[~ties], exp_p[~ties])
     # payload is a permutation of the row's global indices (checksum of checksums)
     assert torch.equal(p.view(torch.int64).sum(dim=1), idx.sum(dim=1))
+
+
+# ---------------------------------------------------------------------------
+# both network kernels (register-direct for rows <= 64 B, pipelined through
+# shared memory otherwise) produce the same bits on every direct-eligible
+# shape; NSG_DIRECT_MAX_MB=0 forces the pipelined kernel in a child process
+# ---------------------------------------------------------------------------
+_BOTH_PATHS = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import oracle
+from paper_2002_05599_b200 import batch
+import torch
+out = {{}}
+rng = np.random.default_rng(77)
+for n in (2, 3, 4, 6, 8, 12, 16):
+    for kdt, pdt in (("uint64", None), ("uint64", "uint32"), ("uint32", None), ("uint32", "uint32"),
+                     ("int64", "uint64")):
+        if np.dtype(kdt).itemsize * n > 64:
+            continue
+        keys = rng.integers(0, 4, size=(3001, n)).astype(kdt)
+        pay = None if pdt is None else rng.integers(0, 2**31, size=(3001, n)).astype(pdt)
+        tk = torch.from_numpy(keys.view(np.int64 if keys.itemsize == 8 else np.int32)).cuda()
+        tk = tk.view(torch.uint64 if kdt == "uint64" else (torch.uint32 if kdt == "uint32" else torch.int64))
+        tp = None
+        if pay is not None:
+            tp = torch.from_numpy(pay.view(np.int64 if pay.itemsize == 8 else np.int32)).cuda()
+            tp = tp.view(torch.uint64 if pay.itemsize == 8 else torch.uint32)
+        for tie in (("ref", "unique") if pay is not None else ("unique",)):
+            for fam in ("best", "bn-l"):
+                k, p = batch.sort_rows(tk, tp, family=fam, tie=tie, descending=(n % 2 == 0))
+                key = f"{{n}}-{{kdt}}-{{pdt}}-{{tie}}-{{fam}}"
+                out[key] = (k.cpu().numpy().tobytes(), None if p is None else p.cpu().numpy().tobytes())
+import pickle
+sys.stdout.buffer.write(pickle.dumps(out))
+"""
+
+
+def test_direct_and_pipelined_kernels_agree(torch):
+    import os
+    import pickle
+    import subprocess
+    import sys
+    root = str(Path(__file__).resolve().parent.parent)
+    code = _BOTH_PATHS.format(root=root)
+    runs = []
+    for env_val in (None, "0"):
+        env = dict(os.environ)
+        if env_val is None:
+            env.pop("NSG_DIRECT_MAX_MB", None)
+        else:
+            env["NSG_DIRECT_MAX_MB"] = env_val
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, timeout=600)
+        assert r.returncode == 0, r.stderr.decode()[-2000:]
+        runs.append(pickle.loads(r.stdout))
+    assert runs[0].keys() == runs[1].keys() and len(runs[0]) > 20
+    for key in runs[0]:
+        assert runs[0][key] == runs[1][key], key

@@ -72,7 +72,17 @@ KernelInfo lookup_dag(int key_bytes, int pay, int mode, int layout) {
 //  keys-only: E = NSG_MERGE_E_KEYS per lane (16: Green-16, n = 32..512;
 //  32: the odd-even merge network of csrc/gen/nets.cuh, n = 32..1024);
 //  with payload: E = 16 per lane (Green-16), n = 32..512.
+#ifndef NSG_MERGE32_ONE_LANE
+#define NSG_MERGE32_ONE_LANE 1
+#endif
 KernelInfo merge_lookup(int n, int key_bytes, int pay, int* lanes_per_row) {
+  if (NSG_MERGE32_ONE_LANE && n == 32 && pay == 0) {
+    // 32 keys on ONE lane: the 185-comparator odd-even merge network of two
+    // Green-16s (csrc/gen/nets.cuh DAG 2), no cross-lane stages
+    *lanes_per_row = 1;
+    return key_bytes == 4 ? info<32, 2, uint32_t, NoPay, MODE_UNIQUE, LAYOUT_SOA, 1>()
+                          : info<32, 2, uint64_t, NoPay, MODE_UNIQUE, LAYOUT_SOA, 1>();
+  }
   const int e = pay == 0 ? NSG_MERGE_E_KEYS : 16;
   if (n % e) return KernelInfo{};
   const int g = n / e;

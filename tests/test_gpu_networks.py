@@ -208,6 +208,24 @@ def test_sort_rows_inplace_and_host_path(torch):
     assert np.array_equal(kt.cpu().numpy(), ek) and np.array_equal(pt.cpu().numpy(), ep)
 
 
+@pytest.mark.parametrize("n,rows", [(8, (1 << 23) + 37), (5, 3_000_001), (16, 700_001)])
+def test_host_path_chunk_plan_large(n, rows, torch):
+    """Host-buffer calls larger than two chunk ramps (ramp up 4 MiB -> 64 MiB
+    chunks, uniform middle, ramp down) equal the device-resident result."""
+    from paper_2002_05599_b200 import batch
+    rng = np.random.default_rng(n)
+    keys = rng.integers(0, 2**64, size=(rows, n), dtype=np.uint64)
+    pay = np.tile(np.arange(n, dtype=np.uint32), (rows, 1))
+    hk, hp = batch.sort_rows(keys, pay)
+    kt = torch.from_numpy(keys.view(np.int64)).cuda().view(torch.uint64)
+    pt = torch.from_numpy(pay.view(np.int32)).cuda().view(torch.uint32)
+    dk, dp = batch.sort_rows(kt, pt)
+    assert np.array_equal(hk, dk.cpu().numpy()) and np.array_equal(hp, dp.cpu().numpy().view(np.uint32))
+    sub = slice(rows - 4000, rows)
+    ek, ep = oracle.typed_sort_rows(keys[sub], pay[sub])
+    assert np.array_equal(hk[sub], ek) and np.array_equal(hp[sub], ep)
+
+
 @pytest.mark.parametrize("rows", [1, 2, 31, 32, 33, 127, 129, 511, 513, 4095, 4097, 65537])
 def test_ragged_row_counts(rows, torch):
     from paper_2002_05599_b200 import batch

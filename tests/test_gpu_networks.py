@@ -359,3 +359,43 @@ def test_direct_and_pipelined_kernels_agree(torch):
     assert runs[0].keys() == runs[1].keys() and len(runs[0]) > 20
     for key in runs[0]:
         assert runs[0][key] == runs[1][key], key
+
+
+# ---------------------------------------------------------------------------
+# randomised cross-check of the whole typed network surface (both kernels:
+# register-direct rows <= 64 B, pipelined otherwise) against the oracle
+# ---------------------------------------------------------------------------
+def _to_dev(torch, a):
+    a = np.ascontiguousarray(a)
+    if a.dtype.kind == "u":
+        sig = {4: np.int32, 8: np.int64}[a.dtype.itemsize]
+        return torch.from_numpy(a.view(sig)).cuda().view({4: torch.uint32, 8: torch.uint64}[a.dtype.itemsize])
+    return torch.from_numpy(a).cuda()
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_randomised_typed_networks_vs_oracle(seed, torch):
+    from paper_2002_05599_b200 import batch
+    rng = np.random.default_rng(9000 + seed)
+    n = int(rng.integers(2, 17))
+    rows = int(rng.choice([1, 7, 33, 1000, 4097, 20011]))
+    kdt = str(rng.choice(["uint32", "uint64", "int32", "int64", "float32"]))
+    pdt = [None, "uint32", "uint64"][int(rng.integers(0, 3))]
+    tie = "ref" if (pdt is not None and rng.integers(0, 2)) else "unique"
+    desc = bool(rng.integers(0, 2))
+    fam = str(rng.choice(["best", "bn-l"]))
+    few = bool(rng.integers(0, 2))  # duplicate-heavy keys: REF-mode payload order is DAG-observable
+    if kdt == "float32":
+        keys = (rng.integers(-3, 4, size=(rows, n)) if few else rng.standard_normal((rows, n)) * 1e3).astype(kdt)
+    else:
+        info = np.iinfo(kdt)
+        keys = (rng.integers(0, 3, size=(rows, n)).astype(kdt) if few else
+                rng.integers(info.min, info.max, size=(rows, n), endpoint=True, dtype=kdt))
+    pay = None if pdt is None else rng.integers(0, 2**31, size=(rows, n)).astype(pdt)
+    ek, ep = oracle.typed_sort_rows(keys, pay, family=fam, descending=desc, unique=tie == "unique")
+    gk, gp = batch.sort_rows(_to_dev(torch, keys), None if pay is None else _to_dev(torch, pay), family=fam,
+                             tie=tie, descending=desc)
+    cfg = (n, rows, kdt, pdt, tie, desc, fam, few)
+    assert np.array_equal(gk.cpu().numpy().view(np.uint8), ek.view(np.uint8)), cfg
+    if pay is not None:
+        assert np.array_equal(gp.cpu().numpy().view(pay.dtype), ep), cfg

@@ -47,6 +47,12 @@
 #ifndef NSG_DEEP_RING_KB
 #define NSG_DEEP_RING_KB 32  // per-warp ring of the deep configuration
 #endif
+#ifndef NSG_MERGE_WARPS
+#define NSG_MERGE_WARPS 16  // warps per CTA of the merge-sorter configurations (measured best of 4/8/12/16)
+#endif
+#ifndef NSG_MERGE_STAGES
+#define NSG_MERGE_STAGES 2  // ring depth of the merge-sorter configurations
+#endif
 #ifndef NSG_DEEP_MIN_ROW
 #define NSG_DEEP_MIN_ROW 32  // rows at least this long get the deep ring
 #endif
@@ -218,10 +224,10 @@ struct NetCfg {
   static constexpr bool DEEP8 = DEEP && NSG_DEEP_WARPS == 4 && NSG_DEEP_RING_KB == 32 && deep8_shape(N, KEB, PEB);
   static constexpr int DEEP_STAGES = ((DEEP8 ? 16 : NSG_DEEP_RING_KB) * 1024) / STAGE_SMEM;
   static constexpr int WANT_STAGES =
-      DEEP ? (DEEP_STAGES > 8 ? 8 : (DEEP_STAGES < 2 ? 2 : DEEP_STAGES)) : (MERGE ? 2 : NSG_STAGES);
+      DEEP ? (DEEP_STAGES > 8 ? 8 : (DEEP_STAGES < 2 ? 2 : DEEP_STAGES)) : (MERGE ? NSG_MERGE_STAGES : NSG_STAGES);
   static constexpr int STAGES = WANT_STAGES <= STAGES_FIT ? WANT_STAGES : (STAGES_FIT >= 2 ? STAGES_FIT : 2);
   static constexpr int WARPS_FIT = SMEM_BUDGET / (STAGES * STAGE_SMEM);
-  static constexpr int WANT_WARPS = DEEP ? (DEEP8 ? 8 : NSG_DEEP_WARPS) : NSG_WARPS;
+  static constexpr int WANT_WARPS = DEEP ? (DEEP8 ? 8 : NSG_DEEP_WARPS) : (MERGE ? NSG_MERGE_WARPS : NSG_WARPS);
   static constexpr int WARPS = WARPS_FIT >= WANT_WARPS ? WANT_WARPS : (WARPS_FIT >= 1 ? WARPS_FIT : 1);
   static constexpr int WARP_SMEM = STAGES * STAGE_SMEM;
   static constexpr int CTA_SMEM = WARPS * WARP_SMEM;

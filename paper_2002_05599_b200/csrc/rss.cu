@@ -36,6 +36,13 @@ namespace {
 
 constexpr uint32_t kLcgM = 2147483647u;
 
+#ifndef NSG_RSS_WARPS
+#define NSG_RSS_WARPS 24  // warps per CTA of the warp kernel, keys-only rows <= 256 items (4/8/12/16/24 swept)
+#endif
+#ifndef NSG_RSS_WARPS_P
+#define NSG_RSS_WARPS_P 4  // same, rows with a payload
+#endif
+
 struct LcgPow {
   uint32_t p[65];
 };
@@ -97,7 +104,7 @@ struct RssCfg {
   static constexpr bool HAS_P = !IsNoPay<P>::value;
   static constexpr int PB = PayBytes<P>::value;
   static constexpr int NMAX_ = NMAX;
-  static constexpr int WARPS = NMAX <= 256 ? 4 : 2;
+  static constexpr int WARPS = NMAX <= 256 ? (HAS_P ? NSG_RSS_WARPS_P : NSG_RSS_WARPS) : 2;
   // per-warp shared memory
   static constexpr int BUF_BYTES = NMAX * (int(sizeof(U)) + PB);
   static constexpr int OFF_A = 0;
@@ -195,7 +202,9 @@ __device__ __forceinline__ void leaf_pad(const WarpBufs<Cfg>& wb, int lo, int c,
 
 template <class U, class P, int NMAX, int DAG, int MODE, int LAYOUT>
 __global__ void __launch_bounds__(RssCfg<U, P, NMAX, DAG, MODE, LAYOUT>::WARPS * 32,
-                                  NMAX <= 256 ? (IsNoPay<P>::value ? 6 : 3) : 2)
+                                  NMAX <= 256 ? (IsNoPay<P>::value ? (24 + NSG_RSS_WARPS - 1) / NSG_RSS_WARPS
+                                                                   : (12 + NSG_RSS_WARPS_P - 1) / NSG_RSS_WARPS_P)
+                                              : 2)
     rss_kernel(const RssParams prm) {
   using Cfg = RssCfg<U, P, NMAX, DAG, MODE, LAYOUT>;
   using E = Elem<U, P>;

@@ -141,12 +141,13 @@ static int64_t env_i64(const char* name, int64_t dflt) {
 // the 2^30 CTA limit: the CTA scheduler streams CTAs in as others retire.
 static int launch_direct(const KernelInfo& k, NetParams prm, cudaStream_t stream) {
   static const int64_t cta_bytes = env_i64("NSG_DIRECT_CTA_KB", 8) << 10;
-  const int64_t rows_per_cta = std::max<int64_t>(256, cta_bytes / k.row_bytes / 256 * 256);
+  constexpr int64_t T = NSG_DIRECT_THREADS;
+  const int64_t rows_per_cta = std::max<int64_t>(T, cta_bytes / k.row_bytes / T * T);
   const int64_t grid = std::min<int64_t>((prm.rows + rows_per_cta - 1) / rows_per_cta, int64_t(1) << 30);
   LaunchGeom g;
-  if (int rc = launch_geom(k.direct_fn, 256, 0, &g)) return rc;
+  if (int rc = launch_geom(k.direct_fn, int(T), 0, &g)) return rc;
   void* args[] = {&prm};
-  NSG_CUDA(cudaLaunchKernel(k.direct_fn, dim3(unsigned(grid)), dim3(256), args, 0, stream));
+  NSG_CUDA(cudaLaunchKernel(k.direct_fn, dim3(unsigned(grid)), dim3(unsigned(T)), args, 0, stream));
   return 0;
 }
 

@@ -3,6 +3,10 @@
 
 #include <cstdint>
 
+#ifndef NSG_DIRECT_THREADS
+#define NSG_DIRECT_THREADS 256  // CTA size of the register-direct kernel (also in net_sort.cuh)
+#endif
+
 namespace nsg {
 
 struct KernelInfo {

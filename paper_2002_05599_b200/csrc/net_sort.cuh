@@ -47,6 +47,9 @@
 #ifndef NSG_DEEP_RING_KB
 #define NSG_DEEP_RING_KB 32  // per-warp ring of the deep configuration
 #endif
+#ifndef NSG_DIRECT_THREADS
+#define NSG_DIRECT_THREADS 256  // CTA size of the register-direct kernel
+#endif
 #ifndef NSG_MERGE_WARPS
 #define NSG_MERGE_WARPS 16  // warps per CTA of the merge-sorter configurations (measured best of 4/8/12/16)
 #endif
@@ -682,7 +685,7 @@ __device__ __forceinline__ void ldg_row(const unsigned char* g, uint32_t (&w)[G:
 }
 
 template <class Cfg>
-__global__ void __launch_bounds__(256) net_direct_kernel(const NetParams p) {
+__global__ void __launch_bounds__(NSG_DIRECT_THREADS) net_direct_kernel(const NetParams p) {
   using U = typename Cfg::U;
   using P = typename Cfg::P;
   using GK = typename Cfg::GK;

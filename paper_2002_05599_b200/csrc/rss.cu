@@ -39,6 +39,9 @@ constexpr uint32_t kLcgM = 2147483647u;
 #ifndef NSG_RSS_WARPS
 #define NSG_RSS_WARPS 24  // warps per CTA of the warp kernel, keys-only rows <= 256 items (4/8/12/16/24 swept)
 #endif
+#ifndef NSG_RSS_TPB
+#define NSG_RSS_TPB 32  // threads per CTA of the thread-per-array kernel (rows <= 32 items; 32/64/128 swept)
+#endif
 #ifndef NSG_RSS_WARPS_P
 #define NSG_RSS_WARPS_P 4  // same, rows with a payload
 #endif
@@ -947,7 +950,7 @@ RssKernel rss_pick_dag(int key_bytes, int pay, int mode, int layout) {
 
 template <class U, class P, int NT, int DAG, int MODE, int LAYOUT>
 RssKernel rss_thread_info() {
-  constexpr int TPB = 64;
+  constexpr int TPB = NSG_RSS_TPB;
   return {reinterpret_cast<const void*>(&rss_thread_kernel<U, P, NT, TPB, DAG, MODE, LAYOUT>),
           TCfg<U, P, NT, TPB>::SMEM, TPB, TPB};
 }

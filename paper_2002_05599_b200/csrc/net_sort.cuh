@@ -47,6 +47,12 @@
 #ifndef NSG_DEEP_RING_KB
 #define NSG_DEEP_RING_KB 32  // per-warp ring of the deep configuration
 #endif
+#ifndef NSG_DEEP_TILE
+#define NSG_DEEP_TILE 8192  // tile bytes of the deep configuration
+#endif
+#ifndef NSG_PAIR_ROWS
+#define NSG_PAIR_ROWS 0  // pipelined kernel: run two rows per network, interleaved
+#endif
 #ifndef NSG_DIRECT_THREADS
 #define NSG_DIRECT_THREADS 256  // CTA size of the register-direct kernel
 #endif
@@ -180,6 +186,14 @@ constexpr bool deep8_shape(int n, int keb, int peb) {
          (keb == 8 && peb == 4 && (n == 3 || n == 5 || n == 9 || n == 10 || n == 15));
 }
 
+// Deep shapes measured faster with 16 KiB tiles (two rows per lane, their
+// networks interleaved comparator by comparator -- sort_elems_pair) in a
+// 48 KiB per-warp ring: Bose-Nelson u64 key + u32 payload at n = 11, 12, 13,
+// 15 (+5-10 %).  (N, DAG, key bytes, payload bytes.)
+constexpr bool wide_shape(int n, int dag, int keb, int peb) {
+  return dag == 1 && keb == 8 && peb == 4 && (n == 11 || n == 12 || n == 13 || n == 15);
+}
+
 // Compile-time configuration of one kernel instance.  G > 1 (merge sorter):
 // a row of G*N items is split into G contiguous sub-rows of N, one per lane;
 // each lane sorts its sub-row with Net<DAG, N>, then the G lanes merge with
@@ -213,7 +227,8 @@ struct NetCfg {
   static constexpr bool MERGE = N > 16 || G > 1;
   static constexpr bool DEEP =
       !MERGE && ROW_BYTES >= NSG_DEEP_MIN_ROW && NSG_STAGES == 3 && NSG_TILE_BYTES == 4096;
-  static constexpr int TILE_BYTES = DEEP ? 8192 : NSG_TILE_BYTES;
+  static constexpr bool WIDE = DEEP && NSG_DEEP_TILE == 8192 && wide_shape(N, DAG, KEB, PEB);
+  static constexpr int TILE_BYTES = WIDE ? 16384 : (DEEP ? NSG_DEEP_TILE : NSG_TILE_BYTES);
   static constexpr int APL_RAW = TILE_BYTES / (32 * ROW_BYTES);
   static constexpr int APL_POW2 = APL_RAW >= 16 ? 16 : APL_RAW >= 8 ? 8 : APL_RAW >= 4 ? 4 : APL_RAW >= 2 ? 2 : 1;
   static constexpr int APL = APL_POW2 > NSG_MAX_APL ? NSG_MAX_APL : APL_POW2;
@@ -224,8 +239,12 @@ struct NetCfg {
   // ring depth and warps per CTA shrink for very long rows (n = 32 / 64)
   static constexpr int SMEM_BUDGET = 200 * 1024;
   static constexpr int STAGES_FIT = (SMEM_BUDGET / 2) / STAGE_SMEM;
-  static constexpr bool DEEP8 = DEEP && NSG_DEEP_WARPS == 4 && NSG_DEEP_RING_KB == 32 && deep8_shape(N, KEB, PEB);
-  static constexpr int DEEP_STAGES = ((DEEP8 ? 16 : NSG_DEEP_RING_KB) * 1024) / STAGE_SMEM;
+  static constexpr bool DEEP8 =
+      DEEP && !WIDE && NSG_DEEP_WARPS == 4 && NSG_DEEP_RING_KB == 32 && deep8_shape(N, KEB, PEB);
+  static constexpr int DEEP_STAGES = ((DEEP8 ? 16 : (WIDE ? 48 : NSG_DEEP_RING_KB)) * 1024) / STAGE_SMEM;
+  // two rows per network (interleaved) -- the WIDE shapes, or every even-APL
+  // instance with the NSG_PAIR_ROWS experiment knob
+  static constexpr bool PAIR = (NSG_PAIR_ROWS || WIDE) && G == 1 && APL % 2 == 0;
   static constexpr int WANT_STAGES =
       DEEP ? (DEEP_STAGES > 8 ? 8 : (DEEP_STAGES < 2 ? 2 : DEEP_STAGES)) : (MERGE ? NSG_MERGE_STAGES : NSG_STAGES);
   static constexpr int STAGES = WANT_STAGES <= STAGES_FIT ? WANT_STAGES : (STAGES_FIT >= 2 ? STAGES_FIT : 2);
@@ -434,6 +453,69 @@ __device__ __forceinline__ void sort_elems(Elem<typename Cfg::U, typename Cfg::P
   }
 }
 
+// Two rows through one network, comparator by comparator (CX applied to row
+// 0's pair, then row 1's): twice the independent compare-exchanges per
+// network level, so one warp per scheduler keeps its ALU pipe fed through
+// networks with few comparators per level (Bose-Nelson).
+template <class E>
+struct RowPair {
+  E a, b;
+};
+template <class CX>
+struct CxPair {
+  template <class E>
+  __device__ __forceinline__ static void cx(RowPair<E>& x, RowPair<E>& y) {
+    CX::cx(x.a, y.a);
+    CX::cx(x.b, y.b);
+  }
+};
+
+template <class Cfg>
+__device__ __forceinline__ void sort_elems_pair(Elem<typename Cfg::U, typename Cfg::P> (&e0)[Cfg::N],
+                                                Elem<typename Cfg::U, typename Cfg::P> (&e1)[Cfg::N],
+                                                const Xform& xf) {
+  using U = typename Cfg::U;
+  using P = typename Cfg::P;
+  using E = Elem<U, P>;
+  constexpr int N = Cfg::N;
+  if (xf.active) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      e0[j].k = to_ord<U>(e0[j].k, xf);
+      e1[j].k = to_ord<U>(e1[j].k, xf);
+      if constexpr (Cfg::HAS_P) {
+        e0[j].p ^= P(xf.pdesc);
+        e1[j].p ^= P(xf.pdesc);
+      }
+    }
+  }
+#if !NSG_NO_NETWORK
+  RowPair<E> v[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    v[j].a = e0[j];
+    v[j].b = e1[j];
+  }
+  Net<Cfg::DAG, N>::template run<CxPair<typename Cfg::CX>>(v);
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    e0[j] = v[j].a;
+    e1[j] = v[j].b;
+  }
+#endif
+  if (xf.active) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      e0[j].k = from_ord<U>(e0[j].k, xf);
+      e1[j].k = from_ord<U>(e1[j].k, xf);
+      if constexpr (Cfg::HAS_P) {
+        e0[j].p ^= P(xf.pdesc);
+        e1[j].p ^= P(xf.pdesc);
+      }
+    }
+  }
+}
+
 template <class Cfg>
 __device__ __forceinline__ void store_row_elems(unsigned char* smk, unsigned char* smp, int r,
                                                 const Elem<typename Cfg::U, typename Cfg::P> (&e)[Cfg::N]) {
@@ -617,8 +699,13 @@ __global__ void __launch_bounds__(Cfg::WARPS * 32, 1) net_sort_kernel(const NetP
 #pragma unroll
       for (int a = 0; a < Cfg::APL; ++a)
         if (a * 32 + lane < vrows) load_row_elems<Cfg>(smk, smp, a * 32 + lane, e[a]);
+      if constexpr (Cfg::PAIR) {
 #pragma unroll
-      for (int a = 0; a < Cfg::APL; ++a) sort_elems<Cfg>(e[a], p.xf);
+        for (int a = 0; a < Cfg::APL; a += 2) sort_elems_pair<Cfg>(e[a], e[a + 1], p.xf);
+      } else {
+#pragma unroll
+        for (int a = 0; a < Cfg::APL; ++a) sort_elems<Cfg>(e[a], p.xf);
+      }
 #if NSG_DIRECT_STORE
 #pragma unroll
       for (int a = 0; a < Cfg::APL; ++a)

@@ -189,9 +189,17 @@ constexpr bool deep8_shape(int n, int keb, int peb) {
 // Deep shapes measured faster with 16 KiB tiles (two rows per lane, their
 // networks interleaved comparator by comparator -- sort_elems_pair) in a
 // 48 KiB per-warp ring: Bose-Nelson u64 key + u32 payload at n = 11, 12, 13,
-// 15 (+5-10 %).  (N, DAG, key bytes, payload bytes.)
+// 15 (+5-10 %; n = 16 measured 17 % slower that way, 12 or
+// 16 KiB tiles alike).  (N, DAG, key bytes, payload bytes.)
+#ifndef NSG_WIDE_TILE
+#define NSG_WIDE_TILE 16384
+#endif
+#ifndef NSG_WIDE_RING_KB
+#define NSG_WIDE_RING_KB 48
+#endif
 constexpr bool wide_shape(int n, int dag, int keb, int peb) {
-  return dag == 1 && keb == 8 && peb == 4 && (n == 11 || n == 12 || n == 13 || n == 15);
+  return dag == 1 && keb == 8 && peb == 4 &&
+         (n == 11 || n == 12 || n == 13 || n == 15);
 }
 
 // Compile-time configuration of one kernel instance.  G > 1 (merge sorter):
@@ -228,7 +236,7 @@ struct NetCfg {
   static constexpr bool DEEP =
       !MERGE && ROW_BYTES >= NSG_DEEP_MIN_ROW && NSG_STAGES == 3 && NSG_TILE_BYTES == 4096;
   static constexpr bool WIDE = DEEP && NSG_DEEP_TILE == 8192 && wide_shape(N, DAG, KEB, PEB);
-  static constexpr int TILE_BYTES = WIDE ? 16384 : (DEEP ? NSG_DEEP_TILE : NSG_TILE_BYTES);
+  static constexpr int TILE_BYTES = WIDE ? NSG_WIDE_TILE : (DEEP ? NSG_DEEP_TILE : NSG_TILE_BYTES);
   static constexpr int APL_RAW = TILE_BYTES / (32 * ROW_BYTES);
   static constexpr int APL_POW2 = APL_RAW >= 16 ? 16 : APL_RAW >= 8 ? 8 : APL_RAW >= 4 ? 4 : APL_RAW >= 2 ? 2 : 1;
   static constexpr int APL = APL_POW2 > NSG_MAX_APL ? NSG_MAX_APL : APL_POW2;
@@ -241,7 +249,7 @@ struct NetCfg {
   static constexpr int STAGES_FIT = (SMEM_BUDGET / 2) / STAGE_SMEM;
   static constexpr bool DEEP8 =
       DEEP && !WIDE && NSG_DEEP_WARPS == 4 && NSG_DEEP_RING_KB == 32 && deep8_shape(N, KEB, PEB);
-  static constexpr int DEEP_STAGES = ((DEEP8 ? 16 : (WIDE ? 48 : NSG_DEEP_RING_KB)) * 1024) / STAGE_SMEM;
+  static constexpr int DEEP_STAGES = ((DEEP8 ? 16 : (WIDE ? NSG_WIDE_RING_KB : NSG_DEEP_RING_KB)) * 1024) / STAGE_SMEM;
   // two rows per network (interleaved) -- the WIDE shapes, or every even-APL
   // instance with the NSG_PAIR_ROWS experiment knob
   static constexpr bool PAIR = (NSG_PAIR_ROWS || WIDE) && G == 1 && APL % 2 == 0;

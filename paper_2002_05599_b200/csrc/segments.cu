@@ -232,9 +232,49 @@ __device__ __forceinline__ void sort_segment_pad16(U* keys, P* pays, int len, co
   }
 }
 
+// len <= M items through the M-channel network with +inf sentinels (exact
+// only when the output order is unique: keys-only / UNIQUE mode)
+template <int M, class U, class P, int DAG, class CX, int XK>
+__device__ __forceinline__ void sort_segment_padm(U* keys, P* pays, int len, const Xform& xf) {
+  constexpr bool HAS_P = !IsNoPay<P>::value;
+  Elem<U, P> v[M];
+#pragma unroll
+  for (int j = 0; j < M; ++j) {
+    if (j < len) {
+      v[j].k = xk_to<XK>(keys[j], xf);
+      if constexpr (HAS_P) v[j].p = xk_pay<XK>(pays[j], xf);
+    } else {
+      v[j].k = U(~U(0));
+      if constexpr (HAS_P) v[j].p = P(~P(0));
+    }
+  }
+  Net<DAG, M>::template run<CX>(v);
+#pragma unroll
+  for (int j = 0; j < M; ++j) {
+    if (j < len) {
+      keys[j] = xk_from<XK>(v[j].k, xf);
+      if constexpr (HAS_P) pays[j] = xk_pay<XK>(v[j].p, xf);
+    }
+  }
+}
+
+// Unique-order modes sort 5..8 items with the padded 8-network: four fewer
+// network bodies in the sort phase (instruction cache) outweigh the extra
+// comparators (cfg4 1.558 -> 1.532 ms; padding 9..10 to 16 or 3..4 to 4 as
+// well measured slower).  REF mode keeps exact lengths (DAG parity).
+#ifndef NSG_SEG_PAD8
+#define NSG_SEG_PAD8 1
+#endif
+
 template <class U, class P, int DAG, class CX, int XK>
 __device__ __forceinline__ void sort_segment_smem(U* keys, P* pays, int len, const Xform& xf) {
   constexpr bool kPad16 = DAG == 0 || !std::is_same<CX, CxRef>::value;
+  if constexpr (NSG_SEG_PAD8 && !std::is_same<CX, CxRef>::value) {
+    if (len >= 5 && len <= 8) {
+      sort_segment_padm<8, U, P, DAG, CX, XK>(keys, pays, len, xf);
+      return;
+    }
+  }
   if constexpr (kPad16) {
     if (len >= 11) {
       sort_segment_pad16<U, P, DAG, CX, XK>(keys, pays, len, xf);

@@ -188,9 +188,10 @@ constexpr bool deep8_shape(int n, int keb, int peb) {
 
 // Deep shapes measured faster with 16 KiB tiles (two rows per lane, their
 // networks interleaved comparator by comparator -- sort_elems_pair) in a
-// 48 KiB per-warp ring: Bose-Nelson u64 key + u32 payload at n = 11, 12, 13,
-// 15 (+5-10 %; n = 16 measured 17 % slower that way, 12 or
-// 16 KiB tiles alike).  (N, DAG, key bytes, payload bytes.)
+// 48 KiB per-warp ring: u64 key + u32 payload, Bose-Nelson n = 11, 12, 13, 15
+// (+5-10 %) and best-known n = 11 (+3 %) (BN n = 16 measured
+// 17 % slower that way with 12 or 16 KiB tiles, best n = 16 no change).
+// (N, DAG, key bytes, payload bytes.)
 #ifndef NSG_WIDE_TILE
 #define NSG_WIDE_TILE 16384
 #endif
@@ -198,8 +199,7 @@ constexpr bool deep8_shape(int n, int keb, int peb) {
 #define NSG_WIDE_RING_KB 48
 #endif
 constexpr bool wide_shape(int n, int dag, int keb, int peb) {
-  return dag == 1 && keb == 8 && peb == 4 &&
-         (n == 11 || n == 12 || n == 13 || n == 15);
+  return keb == 8 && peb == 4 && ((dag == 1 && (n == 11 || n == 12 || n == 13 || n == 15)) || (dag == 0 && n == 11));
 }
 
 // Compile-time configuration of one kernel instance.  G > 1 (merge sorter):

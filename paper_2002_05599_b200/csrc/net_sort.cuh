@@ -183,7 +183,7 @@ __device__ __forceinline__ void word_put(uint32_t* w, int j, uint64_t v) {
 // 64 MiB launch is ramp-bound, 17-19.5 us either way), so it stays at 4.
 constexpr bool deep8_shape(int n, int keb, int peb) {
   return (keb == 8 && peb == 0 && (n == 5 || n == 6 || n == 7 || n == 11 || n == 13 || n == 14)) ||
-         (keb == 8 && peb == 4 && (n == 3 || n == 5 || n == 9 || n == 10 || n == 15));
+         (keb == 8 && peb == 4 && (n == 3 || n == 5 || n == 7 || n == 9 || n == 10 || n == 15));
 }
 
 // Deep shapes measured faster with 16 KiB tiles (two rows per lane, their

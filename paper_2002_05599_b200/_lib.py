@@ -31,7 +31,7 @@ EXPORTS = (
     "nsg_lcg_next", "nsg_fill_splitmix", "nsg_last_error", "nsg_version",
     "nsg_verify_rows", "nsg_verify_segments",
     "nsg_fill_lcg", "nsg_lcg_jump", "nsg_fingerprint_ws_bytes", "nsg_fingerprint", "nsg_fingerprint_rows",
-    "nsg_scan_sorted", "nsg_segments_check",
+    "nsg_scan_sorted", "nsg_segments_check", "nsg_rss_fallback_rows",
 )
 
 
@@ -88,6 +88,7 @@ _SIGS = {
     "nsg_fingerprint_rows": (ctypes.c_int, [_P, ctypes.c_int, _I64, _I64, _I64, ctypes.c_uint64, _P, _P]),
     "nsg_scan_sorted": (ctypes.c_int, [_P, ctypes.c_int, _I64, _I64, _P, _P]),
     "nsg_segments_check": (ctypes.c_int, [_P, _P]),
+    "nsg_rss_fallback_rows": (ctypes.c_ulonglong, [ctypes.c_int]),
     "nsg_last_error": (ctypes.c_char_p, []),
     "nsg_version": (ctypes.c_int, []),
 }

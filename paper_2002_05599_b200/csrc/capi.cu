@@ -193,6 +193,7 @@ using namespace nsg;
 extern "C" {
 
 const char* nsg_last_error(void) { return g_err.c_str(); }
+unsigned long long nsg_rss_fallback_rows(int reset) { return rsslvl_fallback_rows(reset != 0); }
 int nsg_version(void) { return 100; }
 
 uint32_t nsg_lcg_next(uint32_t seed) { return uint32_t((uint64_t(seed) * 48271u) % 2147483647u); }

@@ -31,6 +31,12 @@ int launch_rss_segment_list(const nsg_spec& sp, const uint32_t* offsets, const u
                             uint32_t* overflow, int64_t max_rows, const void* keys_in, void* keys_out,
                             const void* pay_in, void* pay_out, cudaStream_t st);
 
+// rsslvl.cu (level-synchronous RSS, keys-only / UNIQUE rows of 17..256 items)
+bool rsslvl_covers(int64_t n);
+int launch_rsslvl(const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows, int64_t n,
+                  int key_bytes, int pay, uint32_t seed, const Xform& xf, cudaStream_t st);
+unsigned long long rsslvl_fallback_rows(bool reset);
+
 // wmerge.cu
 int launch_wmerge(const nsg_spec& sp, const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows,
                   int64_t n, cudaStream_t st);

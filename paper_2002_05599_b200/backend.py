@@ -63,8 +63,10 @@ def run_sorter_many(spec, rows) -> None:
     sp = make_spec(spec)
     network = spec[0] == registry.KIND_NETWORK
     if _is_torch(rows):
+        import torch
         m, n = _check_item_tensor(rows)
-        rc = l.nsg_run_sorter_many(sp, rows.data_ptr(), m, n, current_stream_handle(rows.device))
+        with torch.cuda.device(rows.device):
+            rc = l.nsg_run_sorter_many(sp, rows.data_ptr(), m, n, current_stream_handle(rows.device))
         check(rc, network=network)
         return
     if not isinstance(rows, np.ndarray) or rows.ndim != 2:
@@ -93,7 +95,9 @@ def swap_pairs(code: int, rows) -> None:
         m, two = _check_item_tensor(rows)
         if two != 2:
             raise ConfigurationError("expected an (m, 2) array of item pairs")
-        check(l.nsg_swap_pairs(int(code), rows.data_ptr(), m, current_stream_handle(rows.device)))
+        import torch
+        with torch.cuda.device(rows.device):
+            check(l.nsg_swap_pairs(int(code), rows.data_ptr(), m, current_stream_handle(rows.device)))
         return
     if rows.ndim != 2 or rows.shape[1] != 2:
         raise ConfigurationError("expected an (m, 2) array of item pairs")
@@ -115,8 +119,9 @@ def classify_block_u64(keys, s0, s1, s2, block=1) -> np.ndarray:
     n = kt.numel()
     tags = torch.empty(n, dtype=torch.uint8, device=kt.device)
     if n:
-        check(l.nsg_classify_block(kt.data_ptr(), n, int(s0), int(s1), int(s2), int(block),
-                                   tags.data_ptr(), current_stream_handle(kt.device)))
+        with torch.cuda.device(kt.device):
+            check(l.nsg_classify_block(kt.data_ptr(), n, int(s0), int(s1), int(s2), int(block),
+                                       tags.data_ptr(), current_stream_handle(kt.device)))
     return tags.cpu().numpy() if host else tags
 
 
@@ -181,18 +186,21 @@ def fill_items(arr, seed: int) -> int:
     n = items.shape[0]
     final = ctypes.c_uint32(0)
     ptr = items.data_ptr() if n else None
-    check(l.nsg_fill_lcg(ptr, 16, ptr + 8 if n else None, 16, n, int(seed) & 0xFFFFFFFF, ctypes.byref(final),
-                         current_stream_handle(items.device)))
+    with torch.cuda.device(items.device):
+        check(l.nsg_fill_lcg(ptr, 16, ptr + 8 if n else None, 16, n, int(seed) & 0xFFFFFFFF,
+                             ctypes.byref(final), current_stream_handle(items.device)))
     if host is not None and n:
         host[...] = items.cpu().numpy().view(np.uint64)
     return int(final.value)
 
 
 def _fp_device(items, z: int, ws, out) -> int:
+    import torch
     l = lib()
     n = items.shape[0]
-    check(l.nsg_fingerprint(items.data_ptr() if n else None, 8, 16, n, int(z) & 0xFFFFFFFFFFFFFFFF,
-                            ws.data_ptr(), ws.numel(), out.data_ptr(), current_stream_handle(items.device)))
+    with torch.cuda.device(items.device):
+        check(l.nsg_fingerprint(items.data_ptr() if n else None, 8, 16, n, int(z) & 0xFFFFFFFFFFFFFFFF,
+                                ws.data_ptr(), ws.numel(), out.data_ptr(), current_stream_handle(items.device)))
     return int(out.item()) & 0xFFFFFFFFFFFFFFFF
 
 
@@ -222,7 +230,9 @@ def check_sorted(arr, n=None) -> bool:
     if nn < 2:
         return True
     out = torch.empty(1, dtype=torch.int32, device=items.device)
-    check(lib().nsg_scan_sorted(items.data_ptr(), 8, 16, nn, out.data_ptr(), current_stream_handle(items.device)))
+    with torch.cuda.device(items.device):
+        check(lib().nsg_scan_sorted(items.data_ptr(), 8, 16, nn, out.data_ptr(),
+                                    current_stream_handle(items.device)))
     return int(out.item()) == 0
 
 

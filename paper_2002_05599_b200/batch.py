@@ -37,6 +37,25 @@ def _is_torch(x) -> bool:
     return type(x).__module__.startswith("torch")
 
 
+def _check_out(out, ref, what: str, device=None) -> None:
+    """An output buffer must match its input's shape and element size, be
+    contiguous and (device path) live on the input's CUDA device."""
+    if out is None:
+        return
+    if tuple(out.shape) != tuple(ref.shape):
+        raise ConfigurationError(f"{what} must have shape {tuple(ref.shape)}, got {tuple(out.shape)}")
+    if device is not None:
+        if not _is_torch(out) or not out.is_cuda or out.device != device:
+            raise ConfigurationError(f"{what} must be a CUDA tensor on {device}")
+        if out.element_size() != ref.element_size() or not out.is_contiguous():
+            raise ConfigurationError(f"{what} must be contiguous with element size {ref.element_size()}")
+    else:
+        if not isinstance(out, np.ndarray) or out.itemsize != ref.itemsize or not out.flags.c_contiguous \
+                or not out.flags.writeable:
+            raise ConfigurationError(f"{what} must be a writeable C-contiguous numpy array "
+                                     f"with item size {ref.itemsize}")
+
+
 def make_order(keys, payload, descending: bool, tie: str) -> DeviceOrder:
     kd = _KEY.get(_dtname(keys))
     if kd is None:
@@ -80,29 +99,40 @@ def sort_rows(keys, payload=None, *, kind: str = "network", family: str = "best"
     sp = make_spec(spec, make_order(keys, payload, descending, tie))
     l = lib()
     if _is_torch(keys):
+        import torch
         if not keys.is_cuda or not keys.is_contiguous():
             raise ConfigurationError("keys must be a contiguous CUDA tensor")
+        if payload is not None and (not _is_torch(payload) or not payload.is_cuda
+                                    or payload.device != keys.device or not payload.is_contiguous()):
+            raise ConfigurationError("payload must be a contiguous CUDA tensor on the keys' device")
+        _check_out(out_keys, keys, "out_keys", keys.device)
+        if out_payload is not None and payload is None:
+            raise ConfigurationError("out_payload given without a payload")
+        _check_out(out_payload, payload, "out_payload", keys.device)
         for t in (keys, payload, out_keys, out_payload):
             if t is not None and t.data_ptr() % 16:
                 raise ConfigurationError("device buffers must be 16-byte aligned")
         ok = out_keys if out_keys is not None else keys.new_empty(keys.shape)
         op = None
         if payload is not None:
-            if not payload.is_cuda or not payload.is_contiguous():
-                raise ConfigurationError("payload must be a contiguous CUDA tensor")
             op = out_payload if out_payload is not None else payload.new_empty(payload.shape)
-        rc = l.nsg_sort_rows(sp, keys.data_ptr(), ok.data_ptr(),
-                             payload.data_ptr() if payload is not None else None,
-                             op.data_ptr() if op is not None else None, rows, n,
-                             current_stream_handle(keys.device))
+        with torch.cuda.device(keys.device):
+            rc = l.nsg_sort_rows(sp, keys.data_ptr(), ok.data_ptr(),
+                                 payload.data_ptr() if payload is not None else None,
+                                 op.data_ptr() if op is not None else None, rows, n,
+                                 current_stream_handle(keys.device))
         check(rc, network=kind == "network")
         return ok, op
     keys = np.ascontiguousarray(keys)
+    _check_out(out_keys, keys, "out_keys")
     ok = out_keys if out_keys is not None else np.empty_like(keys)
     op = None
     if payload is not None:
         payload = np.ascontiguousarray(payload)
+        _check_out(out_payload, payload, "out_payload")
         op = out_payload if out_payload is not None else np.empty_like(payload)
+    elif out_payload is not None:
+        raise ConfigurationError("out_payload given without a payload")
     rc = l.nsg_sort_rows_host(sp, keys.ctypes.data, ok.ctypes.data,
                               payload.ctypes.data if payload is not None else None,
                               op.ctypes.data if op is not None else None, rows, n)
@@ -149,13 +179,34 @@ def sort_segments(offsets, keys, payload=None, *, family: str = "best", swap: st
     import torch
     if not _is_torch(keys) or not keys.is_cuda:
         host = True
-        dev = torch.device("cuda")
-        offsets_t = torch.from_numpy(np.ascontiguousarray(offsets, dtype=np.uint32)).to(dev)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        offs = np.asarray(offsets)
+        if offs.ndim != 1 or offs.size < 1:
+            raise ConfigurationError("offsets must be a 1-D array of nseg+1 entries")
+        if offs.size > 1 and (int(offs.min()) < 0 or int(offs[-1]) >= 1 << 32):
+            raise ConfigurationError("offsets must lie in [0, 2^32)")
+        offsets_t = torch.from_numpy(np.ascontiguousarray(offs, dtype=np.uint32).view(np.int32)).to(dev)
         keys_t = torch.from_numpy(np.ascontiguousarray(keys)).to(dev)
         pay_t = torch.from_numpy(np.ascontiguousarray(payload)).to(dev) if payload is not None else None
     else:
         host = False
         offsets_t, keys_t, pay_t = offsets, keys, payload
+        dev = keys_t.device
+        if not _is_torch(offsets_t) or not offsets_t.is_cuda or offsets_t.device != dev \
+                or offsets_t.dtype not in (torch.int32, torch.uint32) or not offsets_t.is_contiguous() \
+                or offsets_t.dim() != 1:
+            raise ConfigurationError("offsets must be a contiguous 1-D int32/uint32 CUDA tensor on the keys' device")
+        if not keys_t.is_contiguous():
+            raise ConfigurationError("keys must be contiguous")
+        if pay_t is not None and (not _is_torch(pay_t) or not pay_t.is_cuda or pay_t.device != dev
+                                  or not pay_t.is_contiguous()):
+            raise ConfigurationError("payload must be a contiguous CUDA tensor on the keys' device")
+        _check_out(out_keys, keys_t, "out_keys", dev)
+        if out_payload is not None and pay_t is None:
+            raise ConfigurationError("out_payload given without a payload")
+        _check_out(out_payload, pay_t, "out_payload", dev)
+    if pay_t is not None and pay_t.numel() != keys_t.numel():
+        raise ConfigurationError("payload must hold one entry per key")
     nseg = int(offsets_t.numel()) - 1
     nelem = int(keys_t.numel())
     spec = registry.spec_network(family, swap)
@@ -166,15 +217,26 @@ def sort_segments(offsets, keys, payload=None, *, family: str = "best", swap: st
     if pay_t is not None:
         op = out_payload if (out_payload is not None and not host) else torch.empty_like(pay_t)
     ws_bytes = int(l.nsg_segments_ws_bytes(nseg, nelem))
-    ws = workspace if workspace is not None else torch.empty(max(ws_bytes, 1), dtype=torch.uint8,
-                                                              device=keys_t.device)
-    rc = l.nsg_sort_segments(sp, offsets_t.data_ptr(), nseg, keys_t.data_ptr(), ok.data_ptr(),
-                             pay_t.data_ptr() if pay_t is not None else None,
-                             op.data_ptr() if op is not None else None, ws.data_ptr(), ws_bytes,
-                             current_stream_handle(keys_t.device))
-    _check(rc, network=False)
-    if check or host:
-        _check(l.nsg_segments_check(ws.data_ptr(), current_stream_handle(keys_t.device)))
+    if workspace is not None:
+        if not _is_torch(workspace) or not workspace.is_cuda or workspace.device != dev \
+                or not workspace.is_contiguous():
+            raise ConfigurationError("workspace must be a contiguous CUDA tensor on the keys' device")
+        ws = workspace
+        ws_have = int(workspace.numel()) * int(workspace.element_size())
+        if ws_have < ws_bytes:
+            raise ConfigurationError(f"workspace holds {ws_have} bytes, need {ws_bytes} "
+                                     "(nsg_segments_ws_bytes)")
+    else:
+        ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+        ws_have = int(ws.numel())
+    with torch.cuda.device(dev):
+        rc = l.nsg_sort_segments(sp, offsets_t.data_ptr(), nseg, keys_t.data_ptr(), ok.data_ptr(),
+                                 pay_t.data_ptr() if pay_t is not None else None,
+                                 op.data_ptr() if op is not None else None, ws.data_ptr(), ws_have,
+                                 current_stream_handle(dev))
+        _check(rc, network=False)
+        if check or host:
+            _check(l.nsg_segments_check(ws.data_ptr(), current_stream_handle(dev)))
     if host:
         return ok.cpu().numpy(), (op.cpu().numpy() if op is not None else None)
     return ok, op

@@ -324,8 +324,11 @@ int nsg_sort_rows_host(const nsg_spec* sp, const void* keys_in, void* keys_out, 
   char* ko = static_cast<char*>(keys_out);
   const char* pi = static_cast<const char*>(pay_in);
   char* po = static_cast<char*>(pay_out);
-  int64_t c = 0;
-  for (int64_t r0 = 0; r0 < rows; r0 += crow, ++c) {
+  // validate the spec and shape on a zero-row call before any copy is issued
+  if (int rc = nsg_sort_rows(sp, p->buf[0], p->buf[0], pb ? p->buf[0] : nullptr, pb ? p->buf[0] : nullptr, 0, n,
+                             p->s[0]))
+    return rc;
+  auto chunk = [&](int64_t r0, int64_t c) -> int {
     const int64_t rr = std::min<int64_t>(crow, rows - r0);
     cudaStream_t s = p->s[c % kPipeBufs];
     char* dk = static_cast<char*>(p->buf[c % kPipeBufs]);
@@ -335,8 +338,15 @@ int nsg_sort_rows_host(const nsg_spec* sp, const void* keys_in, void* keys_out, 
     if (int rc = nsg_sort_rows(sp, dk, dk, pb ? dp : nullptr, pb ? dp : nullptr, rr, n, s)) return rc;
     NSG_CUDA(cudaMemcpyAsync(ko + size_t(r0) * row_k, dk, size_t(rr) * row_k, cudaMemcpyDeviceToHost, s));
     if (pb) NSG_CUDA(cudaMemcpyAsync(po + size_t(r0) * row_p, dp, size_t(rr) * row_p, cudaMemcpyDeviceToHost, s));
-  }
-  return sync_pipe(p);
+    return 0;
+  };
+  int rc = 0;
+  int64_t c = 0;
+  for (int64_t r0 = 0; r0 < rows && !rc; r0 += crow, ++c) rc = chunk(r0, c);
+  // every error path still drains the streams: no copy may touch the
+  // caller's buffers after this call returns
+  const int rs = sync_pipe(p);
+  return rc ? rc : rs;
 }
 
 int nsg_run_sorter_many_host(const nsg_spec* sp, void* rows, int64_t m, int64_t n) {
@@ -352,16 +362,21 @@ int nsg_run_sorter_many_host(const nsg_spec* sp, void* rows, int64_t m, int64_t 
   HostPipe* p = nullptr;
   if (int rc = get_pipe(size_t(crow) * row_b, &p)) return rc;
   char* h = static_cast<char*>(rows);
-  int64_t c = 0;
-  for (int64_t r0 = 0; r0 < m; r0 += crow, ++c) {
+  if (int rc = nsg_run_sorter_many(sp, p->buf[0], 0, n, p->s[0])) return rc;  // validate before copying
+  auto chunk = [&](int64_t r0, int64_t c) -> int {
     const int64_t rr = std::min<int64_t>(crow, m - r0);
     cudaStream_t s = p->s[c % kPipeBufs];
     char* d = static_cast<char*>(p->buf[c % kPipeBufs]);
     NSG_CUDA(cudaMemcpyAsync(d, h + size_t(r0) * row_b, size_t(rr) * row_b, cudaMemcpyHostToDevice, s));
     if (int rc = nsg_run_sorter_many(sp, d, rr, n, s)) return rc;
     NSG_CUDA(cudaMemcpyAsync(h + size_t(r0) * row_b, d, size_t(rr) * row_b, cudaMemcpyDeviceToHost, s));
-  }
-  return sync_pipe(p);
+    return 0;
+  };
+  int rc = 0;
+  int64_t c = 0;
+  for (int64_t r0 = 0; r0 < m && !rc; r0 += crow, ++c) rc = chunk(r0, c);
+  const int rs = sync_pipe(p);
+  return rc ? rc : rs;
 }
 
 int nsg_swap_pairs(int code, void* pairs, int64_t m, void* stream) {

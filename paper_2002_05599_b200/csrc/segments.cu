@@ -538,7 +538,8 @@ int launch_segments(const nsg_spec& sp, const uint32_t* offsets, int64_t nseg, c
   if (nseg >= (int64_t(1) << 32)) return fail(NSG_ERR_SPEC, "segment count must fit in uint32");
   if (ws_bytes < 16 || !ws) return fail(NSG_ERR_SPEC, "segmented sort needs a workspace (nsg_segments_ws_bytes)");
   uint32_t* w = static_cast<uint32_t*>(ws);
-  const uint32_t cap = uint32_t((ws_bytes - 16) / 4);
+  const uint64_t cap64 = uint64_t((ws_bytes - 16) / 4);
+  const uint32_t cap = cap64 > 0xffffffffull ? 0xffffffffu : uint32_t(cap64);
   cudaError_t e = cudaMemsetAsync(ws, 0, 16, st);
   if (e != cudaSuccess) return fail(NSG_ERR_CUDA, "memset: %s", cudaGetErrorString(e));
   const int kb = key_bytes_of(sp.key_dtype);

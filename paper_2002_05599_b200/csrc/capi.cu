@@ -193,7 +193,9 @@ using namespace nsg;
 extern "C" {
 
 const char* nsg_last_error(void) { return g_err.c_str(); }
-unsigned long long nsg_rss_fallback_rows(int reset) { return rsslvl_fallback_rows(reset != 0); }
+unsigned long long nsg_rss_fallback_rows(int reset) {
+  return rsslvl_fallback_rows(reset != 0) + pksort_fallback_rows(reset != 0);
+}
 int nsg_version(void) { return 100; }
 
 uint32_t nsg_lcg_next(uint32_t seed) { return uint32_t((uint64_t(seed) * 48271u) % 2147483647u); }
@@ -227,6 +229,11 @@ int nsg_sort_rows(const nsg_spec* sp, const void* keys_in, void* keys_out, const
     }
     if (sp->payload_dtype != NSG_PAY_NONE && sp->tie_mode != NSG_TIE_UNIQUE)
       return fail(NSG_ERR_SPEC, "the merge sorter orders payloads lexicographically: use tie_mode UNIQUE");
+    // keys-only n = 32: one lane per row with the 185-comparator merge network
+    // (no cross-lane traffic) measures faster than the warp sorter
+    const bool one_lane32 = n == 32 && sp->payload_dtype == NSG_PAY_NONE;
+    if (pksort_covers(n) && !one_lane32 && !env_flag("NSG_MERGE_LEGACY"))  // packed 32-bit words, TMA-staged groups
+      return launch_pksort(keys_in, keys_out, pay_in, pay_out, rows, n, kb, sp->payload_dtype, make_xform(*sp), st);
     int g = 0;
     const KernelInfo mk = merge_lookup(int(n), kb, sp->payload_dtype, &g);
     if (mk.fn) {  // G lanes per row: sub-row networks + cross-lane bitonic merge

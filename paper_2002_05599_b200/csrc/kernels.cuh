@@ -15,6 +15,8 @@ Xform make_xform(const nsg_spec& sp);
 // cached per (device, kernel): sets the dynamic-smem attribute once and
 // returns resident CTAs per SM and the SM count
 int kernel_residency(const void* fn, int threads, int smem, int* ctas_per_sm, int* sms);
+// environment A/B switch: set and not "0" (misc.cu)
+bool env_flag(const char* name);
 
 // misc.cu
 int launch_swap_pairs(void* pairs, int64_t m, cudaStream_t st);
@@ -36,6 +38,12 @@ bool rsslvl_covers(int64_t n);
 int launch_rsslvl(const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows, int64_t n,
                   int key_bytes, int pay, uint32_t seed, const Xform& xf, cudaStream_t st);
 unsigned long long rsslvl_fallback_rows(bool reset);
+
+// pksort.cu (packed-key warp sorter: merge kind, keys-only / UNIQUE rows of 17..256 items)
+bool pksort_covers(int64_t n);
+int launch_pksort(const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows, int64_t n,
+                  int key_bytes, int pay, const Xform& xf, cudaStream_t st);
+unsigned long long pksort_fallback_rows(bool reset);
 
 // wmerge.cu
 int launch_wmerge(const nsg_spec& sp, const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows,

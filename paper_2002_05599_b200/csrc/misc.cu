@@ -2,9 +2,16 @@
 // swap_pairs (ns_cswap_dyn, netsort_core.c:106-118), classify_block
 // (ns_classify_block, netsort_core.c:270-300) and the counter-based input
 // generator used by the benchmarks and tests.
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace nsg {
+
+bool env_flag(const char* name) {  // A/B switches (tests, tuning)
+  const char* e = getenv(name);
+  return e && e[0] && e[0] != '0';
+}
 
 // One conditional swap per pair of packed {key, ref} items: exchange iff
 // right.key < left.key (strict; equal keys stay) -- every swap code.
@@ -39,7 +46,7 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   return x ^ (x >> 31);
 }
 
-// out[i] = splitmix64(seed ^ (first + i) * golden) -- see oracle/gen.py
+// out[i] = splitmix64(seed + (first + i) * golden) -- restated by oracle.splitmix (oracle/__init__.py)
 __global__ void fill_splitmix_kernel(void* out, int64_t count, int elem_bytes, uint64_t seed, uint64_t first) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count;
        i += int64_t(gridDim.x) * blockDim.x) {

@@ -1,0 +1,582 @@
+// Packed-key warp sorter for rows of 17..256 items (the merge sorter's
+// keys-only / UNIQUE path, north star (b)+(c)).
+//
+// The reference sorts each array with networks up to 16 items and with its
+// merge / sample sorts above that (netsort_core.c:270-391, smallsort.py).
+// For keys-only and UNIQUE rows the output is the unique sorted order, so the
+// GPU is free to choose how it gets there.  This kernel spends its issue slots
+// on 32-bit words instead of 64-bit keys:
+//
+//  * staging: each warp owns a ring of 3..8 buffers of W = 32*E element
+//    slots.  One lane moves a whole group of R = W / NR consecutive rows
+//    (NR = pow2 >= n) global -> shared with ONE TMA bulk copy completing on
+//    the buffer's mbarrier, up to six groups ahead of the compute; the sorted
+//    group leaves shared -> global with one bulk store.  No per-element load or
+//    store instructions are issued for the data path.
+//  * packing: lane ll of the L = NR / E lanes of a row reads E keys, maps
+//    them to the order-preserving space and builds 32-bit packed words: the
+//    key bits below the row's common prefix (clz of the OR of k ^ k_row0),
+//    truncated to 32 - log2(NR) bits, with the element's column in the low
+//    bits.  Packed words are unique per row and ordered like the keys.
+//  * sorting: each lane sorts its E words with the best-known network
+//    (Green's 60-comparator 16-sorter at E = 16), then log2(L) bitonic merge
+//    levels combine lanes: one "flip" exchange and the half-cleaners across
+//    lanes by shuffle, the in-lane half-cleaners in registers.  A 32-bit
+//    compare-exchange is two VIMNMX.
+//  * output: the sorted words are transposed through a padded shared array
+//    (conflict-free both ways) to a striped layout, the full keys (and
+//    payloads) gathered by the packed column index from the staged row and
+//    written back in place for the bulk store.
+//
+// Exactness: packed words tie only when two keys agree on every kept bit.
+// Sorted neighbours with equal packed prefixes trigger a full (key, payload)
+// order check of their rows; a row that fails it is re-sorted exactly (warp
+// bitonic sort on the full items, wsort.cuh).  The output is therefore always
+// the unique sorted order; only the speed depends on the data.
+#include "bulk.cuh"
+#include "common.cuh"
+#include "gen/nets.cuh"
+#include "kernels.cuh"
+#include "wsort.cuh"
+
+namespace nsg {
+
+namespace {
+
+#ifndef NSG_PK_E
+#define NSG_PK_E 16  // packed words per lane
+#endif
+#ifndef NSG_PK_WARPS
+#define NSG_PK_WARPS 4  // warps per CTA (independent: no CTA barrier)
+#endif
+#ifndef NSG_PK_RING_BYTES
+#define NSG_PK_RING_BYTES 16384  // staging ring per warp: loads in flight ~ (ring - 2 buffers)
+#endif
+
+__device__ unsigned long long g_pk_fallback_rows;  // diagnostics: rows re-sorted exactly
+
+struct PkParams {
+  const void* k_in;
+  void* k_out;
+  const void* p_in;
+  void* p_out;
+  int64_t rows;
+  int n;
+  int bulk;  // TMA bulk copies allowed (16-byte aligned group chunks)
+  uint32_t one, neg1;  // 1 and ~0, opaque to the compiler (PipeK)
+  Xform xf;
+};
+
+__host__ __device__ constexpr int pk_ilog2(int x) { return x <= 1 ? 0 : 1 + pk_ilog2(x >> 1); }
+
+template <class U, class P, int LOGNR, int E>
+struct PkCfg {
+  static constexpr bool HAS_P = !IsNoPay<P>::value;
+  static constexpr int PB = PayBytes<P>::value;
+  static constexpr int NR = 1 << LOGNR;   // slots per row
+  static constexpr int W = 32 * E;        // slots per warp
+  static constexpr int R = W / NR;        // rows per group
+  static constexpr int L = NR / E;        // lanes per row
+  static constexpr int LOGL = pk_ilog2(L);
+  static constexpr int S = NR + L;        // padded row stride of the transpose array (words)
+  static_assert(R >= 1 && L >= 1 && L <= 32, "row geometry");
+  static constexpr int KB = W * int(sizeof(U));
+  static constexpr int PBB = W * PB;
+  // ring depth: one buffer being sorted, one draining its bulk store, the
+  // rest (>= 1) loading ahead -- HBM latency x bandwidth per SM wants
+  // ~64 KB of loads in flight, so deeper rings for smaller groups
+  static constexpr int NB_RAW = NSG_PK_RING_BYTES / (KB + PBB);
+  static constexpr int NB = NB_RAW < 3 ? 3 : NB_RAW > 8 ? 8 : NB_RAW;
+  static constexpr int AHEAD = NB - 2;  // groups loading ahead of the one being sorted
+  static constexpr int OFF_K = 0;
+  static constexpr int OFF_P = OFF_K + NB * KB;
+  static constexpr int OFF_PA = OFF_P + NB * PBB;
+  static constexpr int OFF_BAR = (OFF_PA + R * S * 4 + 7) / 8 * 8;
+  static constexpr int WARP_SMEM = (OFF_BAR + NB * 8 + 127) / 128 * 128;
+  static constexpr int WARPS = NSG_PK_WARPS;
+  static constexpr int CTA_SMEM = WARPS * WARP_SMEM;
+};
+
+// Compare-exchanges on two execution pipes.  A 32-bit compare-exchange is two
+// VIMNMX on the ALU pipe (reciprocal throughput 2 cycles per SMSP) and the
+// sorter is ALU-bound while the FMA pipe idles.  With lo = min(a, b) the max
+// is a + b - lo (mod 2^32): two IMADs.  The constants 1 and ~0 arrive as
+// launch parameters so the compiler cannot fold the IMADs back into ALU adds.
+struct PipeK {
+  uint32_t one, neg1;
+};
+__device__ __forceinline__ uint32_t mad_lo(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+struct CxAlu {  // min + max: two ALU instructions
+  __device__ __forceinline__ static void cx(uint32_t& a, uint32_t& b, const PipeK&) {
+    const uint32_t lo = min(a, b), hi = max(a, b);
+    a = lo;
+    b = hi;
+  }
+};
+struct CxFma {  // min on the ALU pipe, max = a + b - min on the FMA pipe
+  __device__ __forceinline__ static void cx(uint32_t& a, uint32_t& b, const PipeK& k) {
+    const uint32_t lo = min(a, b);
+    const uint32_t t = mad_lo(a, k.one, b);
+    b = mad_lo(lo, k.neg1, t);
+    a = lo;
+  }
+};
+
+#ifndef NSG_PK_NET_FMA
+#define NSG_PK_NET_FMA 1  // in-lane sorting network on CxFma
+#endif
+#ifndef NSG_PK_HC_FMA
+#define NSG_PK_HC_FMA 1  // leading half-cleaner stages (of log2 E) on CxFma
+#endif
+
+template <int E>
+__device__ __forceinline__ void lane_sort(uint32_t (&v)[E], const PipeK& k) {
+  using CX = typename std::conditional<NSG_PK_NET_FMA != 0, CxFma, CxAlu>::type;
+  if constexpr (E == 32) {
+    Net<2, 32>::template run_k<CX>(v, k);  // odd-even merge of two Green-16s (185 comparators)
+  } else {
+    Net<0, E>::template run_k<CX>(v, k);
+  }
+}
+
+template <int E>
+__device__ __forceinline__ void half_clean(uint32_t (&v)[E], const PipeK& k) {
+  int stage = 0;
+#pragma unroll
+  for (int j = E / 2; j > 0; j >>= 1, ++stage) {
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+      if ((r & j) == 0) {
+        if (stage < NSG_PK_HC_FMA) {
+          CxFma::cx(v[r], v[r | j], k);
+        } else {
+          CxAlu::cx(v[r], v[r | j], k);
+        }
+      }
+    }
+  }
+}
+
+// representation change: flip ? ~v : v, as one IMAD per word
+template <int E>
+__device__ __forceinline__ void pk_conv(uint32_t (&v)[E], bool flip, const PipeK& k) {
+  const uint32_t m = flip ? k.neg1 : k.one;
+  const uint32_t a = flip ? k.neg1 : 0u;
+#pragma unroll
+  for (int r = 0; r < E; ++r) v[r] = mad_lo(v[r], m, a);
+}
+
+// log2(L) bitonic merge levels over the L lanes of a row (blocked layout:
+// lane ll holds sorted positions ll*E .. ll*E+E-1 of its run).
+//
+// In a cross-lane step the lower lane of each pair keeps min(a, b) and the
+// upper one max(a, b).  The upper lane holds its words complemented during
+// that step, so both compute min(own, ~partner) -- one VIMNMX instead of a
+// min/max pair selected by role -- and the complements (representation
+// changes between steps, ~partner) are IMADs on the FMA pipe.
+template <int E, int L>
+__device__ __forceinline__ void merge_lanes32(uint32_t (&v)[E], int ll, const PipeK& k) {
+#pragma unroll
+  for (int kl = 2; kl <= L; kl <<= 1) {
+    bool cur = false;  // this lane's words are complemented
+    {
+      const bool up = (ll & (kl >> 1)) != 0;
+      pk_conv<E>(v, cur != up, k);
+      cur = up;
+      uint32_t o[E];
+#pragma unroll
+      for (int r = 0; r < E; ++r) o[r] = __shfl_xor_sync(0xffffffffu, v[E - 1 - r], kl - 1);
+#pragma unroll
+      for (int r = 0; r < E; ++r) v[r] = min(v[r], mad_lo(o[r], k.neg1, k.neg1));
+    }
+#pragma unroll
+    for (int d = kl >> 2; d >= 1; d >>= 1) {
+      const bool up = (ll & d) != 0;
+      pk_conv<E>(v, cur != up, k);
+      cur = up;
+      uint32_t o[E];
+#pragma unroll
+      for (int r = 0; r < E; ++r) o[r] = __shfl_xor_sync(0xffffffffu, v[r], d);
+#pragma unroll
+      for (int r = 0; r < E; ++r) v[r] = min(v[r], mad_lo(o[r], k.neg1, k.neg1));
+    }
+    pk_conv<E>(v, cur, k);
+    half_clean<E>(v, k);
+  }
+}
+
+template <class T>
+__device__ __forceinline__ T shfl_xor_t(T v, int m) {
+  if constexpr (sizeof(T) == 8) {
+    const uint32_t lo = __shfl_xor_sync(0xffffffffu, uint32_t(v), m);
+    const uint32_t hi = __shfl_xor_sync(0xffffffffu, uint32_t(uint64_t(v) >> 32), m);
+    return T(uint64_t(lo) | (uint64_t(hi) << 32));
+  } else {
+    return T(__shfl_xor_sync(0xffffffffu, uint32_t(v), m));
+  }
+}
+template <class T>
+__device__ __forceinline__ T shfl_up_t(T v, int d) {
+  if constexpr (sizeof(T) == 8) {
+    const uint32_t lo = __shfl_up_sync(0xffffffffu, uint32_t(v), d);
+    const uint32_t hi = __shfl_up_sync(0xffffffffu, uint32_t(uint64_t(v) >> 32), d);
+    return T(uint64_t(lo) | (uint64_t(hi) << 32));
+  } else {
+    return T(__shfl_up_sync(0xffffffffu, uint32_t(v), d));
+  }
+}
+
+// upper 32 bits of (x << cp), 0 <= cp < bits(U); c2 = max(cp - 32, 0):
+// a clamped funnel shift (shift amount capped at 32) then a plain shift
+__device__ __forceinline__ uint32_t top32c(uint32_t x, int cp, int) { return x << cp; }
+__device__ __forceinline__ uint32_t top32c(uint64_t x, int cp, int c2) {
+  return __funnelshift_lc(uint32_t(x), uint32_t(x >> 32), unsigned(cp)) << c2;
+}
+__device__ __forceinline__ int clz_t(uint32_t x) { return __clz(int(x)); }
+__device__ __forceinline__ int clz_t(uint64_t x) { return __clzll((long long)x); }
+
+template <class U, class P>
+__device__ __forceinline__ bool item_lt(U bk, const P& bp, U ak, const P& ap) {
+  if constexpr (IsNoPay<P>::value) {
+    return key_lt(bk, ak);
+  } else {
+    return lex_lt(bk, bp, ak, ap);
+  }
+}
+
+// Exact in-place re-sort of one staged row (raw keys) by the whole warp.
+template <class U, class P>
+__device__ __noinline__ void pk_exact_row(U* rk, P* rp, int n, const Xform xf, int lane) {
+  Elem<U, P> v[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int i = lane * 8 + r;
+    if (i < n) {
+      v[r].k = xf.active ? to_ord<U>(rk[i], xf) : rk[i];
+      if constexpr (!IsNoPay<P>::value) v[r].p = xf.active ? P(rp[i] ^ P(xf.pdesc)) : rp[i];
+    } else {
+      v[r].k = U(~U(0));
+      if constexpr (!IsNoPay<P>::value) v[r].p = P(~P(0));
+    }
+  }
+  __syncwarp();
+  bitonic_warp<U, P, 8>(v, lane);
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int i = lane * 8 + r;
+    if (i < n) {
+      rk[i] = xf.active ? from_ord<U>(v[r].k, xf) : v[r].k;
+      if constexpr (!IsNoPay<P>::value) rp[i] = xf.active ? P(v[r].p ^ P(xf.pdesc)) : v[r].p;
+    }
+  }
+  __syncwarp();
+}
+
+// FULL: n == NR (no padding slots) -- the validity tests drop out; rows past
+// the end of the batch in the last group are sorted as garbage, never stored.
+template <class U, class P, int LOGNR, int E, bool FULL>
+__global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParams prm) {
+  using C = PkCfg<U, P, LOGNR, E>;
+  constexpr int NR = C::NR, R = C::R, L = C::L, LOGL = C::LOGL, W = C::W, S = C::S, NB = C::NB;
+  constexpr bool HAS_P = C::HAS_P;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  unsigned char* wsm = smem_raw + warp * C::WARP_SMEM;
+  U* kbuf = reinterpret_cast<U*>(wsm + C::OFF_K);
+  P* pbuf = reinterpret_cast<P*>(wsm + C::OFF_P);
+  uint32_t* pa = reinterpret_cast<uint32_t*>(wsm + C::OFF_PA);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(wsm + C::OFF_BAR);
+  const U* kin = static_cast<const U*>(prm.k_in);
+  const P* pin = static_cast<const P*>(prm.p_in);
+  U* kout = static_cast<U*>(prm.k_out);
+  P* pout = static_cast<P*>(prm.p_out);
+  const int n = prm.n;
+  const int64_t rows = prm.rows;
+  const Xform xf = prm.xf;
+  const PipeK kk{prm.one, prm.neg1};
+  const int g = lane >> LOGL;       // row of the group this lane serves
+  const int ll = lane & (L - 1);    // lane within the row
+  const int64_t groups = (rows + R - 1) / R;
+  const int64_t gw = int64_t(blockIdx.x) * C::WARPS + warp;
+  const int64_t GW = int64_t(gridDim.x) * C::WARPS;
+
+  if (lane == 0) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) mbar_init(&bar[b], 1);
+    mbar_init_fence();
+  }
+  __syncwarp();
+
+  auto rows_in = [&](int64_t grp) -> int {
+    const int64_t left = rows - grp * R;
+    return left < R ? int(left) : R;
+  };
+  auto bulk_ok = [&](int rin) -> bool {
+    const int64_t cnt = int64_t(rin) * n;
+    return prm.bulk && (cnt * int64_t(sizeof(U))) % 16 == 0 && (cnt * C::PB) % 16 == 0;
+  };
+  auto issue = [&](int64_t grp, int b) {
+    const int rin = rows_in(grp);
+    if (lane == 0 && bulk_ok(rin)) {
+      const int64_t base = grp * R * int64_t(n);
+      const unsigned kbytes = unsigned(rin * n * int(sizeof(U)));
+      const unsigned pbytes = unsigned(rin * n * C::PB);
+      mbar_expect_tx(&bar[b], kbytes + pbytes);
+      bulk_g2s(kbuf + b * W, kin + base, kbytes, &bar[b]);
+      if constexpr (HAS_P) bulk_g2s(pbuf + b * W, pin + base, pbytes, &bar[b]);
+    }
+  };
+
+#pragma unroll
+  for (int a = 0; a < C::AHEAD; ++a) {
+    if (gw + a * GW < groups) issue(gw + a * GW, a);
+  }
+  uint32_t phases = 0;
+  int b = 0;                // buffer of the group being sorted
+  int bn = C::AHEAD % NB;   // buffer the next load goes to
+  for (int64_t grp = gw; grp < groups; grp += GW) {
+    const int64_t nxt = grp + C::AHEAD * GW;
+    // buffer bn last held the group two iterations back: its bulk store must
+    // have finished reading shared memory (the previous group's may still run)
+    if (lane == 0) bulk_wait_read<1>();
+    __syncwarp();
+    if (nxt < groups) issue(nxt, bn);
+    bn = bn + 1 == NB ? 0 : bn + 1;
+    U* fk = kbuf + b * W;
+    P* fp = pbuf + b * W;
+    const int rin = rows_in(grp);
+    const int cnt = rin * n;
+    const int64_t base = grp * R * int64_t(n);
+    const bool bk = bulk_ok(rin);
+    if (bk) {
+      mbar_wait_parity(&bar[b], (phases >> b) & 1u);
+      phases ^= 1u << b;
+    } else {  // unaligned chunk (odd 4-byte rows, the grid's tail): lanes copy
+      for (int i = lane; i < cnt; i += 32) {
+        fk[i] = kin[base + i];
+        if constexpr (HAS_P) fp[i] = pin[base + i];
+      }
+      __syncwarp();
+    }
+
+    // ---- 1. packed words -----------------------------------------------------
+    // lane (g, ll) owns columns pos = ll + L*r, r < rl, of row g; the
+    // loads below stay inside the buffer for every r, so they are unconditional
+    const bool rowv = g < rin;
+    U* rk = fk + g * n;
+    P* rp = fp + g * n;
+    const int rl = FULL ? E : rowv ? (n - ll + L - 1) >> LOGL : 0;  // valid r of this lane
+    uint32_t pk[E];
+    if (!xf.flt) {
+      // integer keys: ord(x) = x ^ M.  The common prefix of x ^ first is the
+      // same in both spaces, and the shifted top word of ord(x) is the shifted
+      // top word of x xor that of M, so the transform costs one XOR per row.
+      const U M = U(xf.sign_or ^ xf.kdesc);
+      const U f = rk[0];
+      U x[E];
+      U acc = U(0);
+#pragma unroll
+      for (int r = 0; r < E; ++r) {
+        x[r] = rk[ll + L * r];
+        if (FULL || r < rl) acc |= x[r] ^ f;
+      }
+#pragma unroll
+      for (int m = 1; m < L; m <<= 1) acc |= shfl_xor_t<U>(acc, m);
+      const int cp = acc ? clz_t(acc) : 0;
+      const int c2 = cp > 32 ? cp - 32 : 0;
+      const uint32_t K0 = (top32c(M, cp, c2) & ~uint32_t(NR - 1)) | uint32_t(ll);
+#pragma unroll
+      for (int r = 0; r < E; ++r) {
+        const uint32_t w = (top32c(x[r], cp, c2) & ~uint32_t(NR - 1)) ^ (K0 + uint32_t(L * r));
+        pk[r] = (FULL || r < rl) ? w : 0xffffffffu;
+      }
+    } else {  // float keys: the full order-preserving map per element
+      const U first = to_ord<U>(rk[0], xf);
+      U x[E];
+      U acc = U(0);
+#pragma unroll
+      for (int r = 0; r < E; ++r) {
+        x[r] = to_ord<U>(rk[ll + L * r], xf);
+        if (FULL || r < rl) acc |= x[r] ^ first;
+      }
+#pragma unroll
+      for (int m = 1; m < L; m <<= 1) acc |= shfl_xor_t<U>(acc, m);
+      const int cp = acc ? clz_t(acc) : 0;
+      const int c2 = cp > 32 ? cp - 32 : 0;
+#pragma unroll
+      for (int r = 0; r < E; ++r) {
+        const uint32_t w = (top32c(x[r], cp, c2) & ~uint32_t(NR - 1)) | uint32_t(ll + L * r);
+        pk[r] = (FULL || r < rl) ? w : 0xffffffffu;
+      }
+    }
+
+    // ---- 2. sort: in-lane network + bitonic merges across the row's lanes ----
+    lane_sort<E>(pk, kk);
+    merge_lanes32<E, L>(pk, ll, kk);
+
+    // ---- 3. sorted neighbours with equal packed prefixes? ---------------------
+    bool tied;
+    {
+      const int lim = rowv ? n - ll * E : 0;  // sorted positions r < lim are real items
+      bool eq = false;
+#pragma unroll
+      for (int r = 0; r + 1 < E; ++r) eq |= (FULL || r + 1 < lim) && ((pk[r] ^ pk[r + 1]) >> LOGNR) == 0u;
+      const uint32_t prev = __shfl_up_sync(0xffffffffu, pk[E - 1], 1);
+      eq |= ll > 0 && (FULL || lim > 0) && ((prev ^ pk[0]) >> LOGNR) == 0u;
+      tied = __ballot_sync(0xffffffffu, eq) != 0u;
+    }
+
+    // ---- 4. transpose blocked -> striped, gather the full items --------------
+    // sorted position q = ll + L*r sits at pr[q + q/E] (one pad word per E);
+    // q/E = (L*r)/E because ll < L <= E
+    uint32_t* pr = pa + g * S;
+#pragma unroll
+    for (int r = 0; r < E; ++r) pr[ll * (E + 1) + r] = pk[r];
+    __syncwarp();
+    U ok[E];
+    P op[E];
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+      if (FULL || r < rl) {
+        const uint32_t idx = pr[ll + L * r + (L * r) / E] & uint32_t(NR - 1);
+        ok[r] = rk[idx];
+        if constexpr (HAS_P) op[r] = rp[idx];
+      }
+    }
+    __syncwarp();  // every gather is done before the staged rows are overwritten
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+      if (FULL || r < rl) {
+        rk[ll + L * r] = ok[r];
+        if constexpr (HAS_P) rp[ll + L * r] = op[r];
+      }
+    }
+    __syncwarp();
+
+    // ---- 5. rows with packed ties: full (key, payload) order check of every
+    //         sorted neighbour pair in the staged output; failures re-sorted
+    //         exactly (rare: distinct keys agreeing on every kept bit) ---------
+    unsigned bad_rows = 0;
+    if (tied) {
+      const U M = U(xf.sign_or ^ xf.kdesc);
+      auto kord = [&](U v) -> U { return xf.flt ? to_ord<U>(v, xf) : U(v ^ M); };
+      bool bad = false;
+#pragma unroll
+      for (int r = 0; r < E; ++r) {
+        const int q = ll + L * r;
+        if ((FULL ? rowv : r < rl) && q > 0) {
+          P a{}, bq{};
+          if constexpr (HAS_P) {
+            a = P(rp[q - 1] ^ P(xf.pdesc));
+            bq = P(op[r] ^ P(xf.pdesc));
+          }
+          bad |= item_lt<U, P>(kord(ok[r]), bq, kord(rk[q - 1]), a);
+        }
+      }
+      const unsigned bm = __ballot_sync(0xffffffffu, bad);
+#pragma unroll
+      for (int gg = 0; gg < R; ++gg) {
+        if ((bm >> (gg * L)) & (L == 32 ? 0xffffffffu : ((1u << L) - 1u))) bad_rows |= 1u << gg;
+      }
+    }
+
+    while (bad_rows) {
+      const int gi = __ffs(int(bad_rows)) - 1;
+      bad_rows &= bad_rows - 1;
+      if (lane == 0) atomicAdd(&g_pk_fallback_rows, 1ull);
+      pk_exact_row<U, P>(fk + gi * n, fp + gi * n, n, xf, lane);
+    }
+
+    // ---- 6. store -----------------------------------------------------------
+    if (bk) {
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        bulk_s2g(kout + base, fk, unsigned(cnt * int(sizeof(U))));
+        if constexpr (HAS_P) bulk_s2g(pout + base, fp, unsigned(cnt * C::PB));
+        bulk_commit();
+      }
+    } else {
+      for (int i = lane; i < cnt; i += 32) {
+        kout[base + i] = fk[i];
+        if constexpr (HAS_P) pout[base + i] = fp[i];
+      }
+    }
+    __syncwarp();
+    b = b + 1 == NB ? 0 : b + 1;
+  }
+  if (lane == 0) bulk_wait<0>();
+}
+
+template <class U, class P>
+const void* pk_fn(int lognr, bool full, int* smem) {
+  switch (lognr) {
+#define NSG_PK_CASE(LG)                                                                        \
+  case LG:                                                                                     \
+    *smem = PkCfg<U, P, LG, NSG_PK_E>::CTA_SMEM;                                               \
+    return full ? reinterpret_cast<const void*>(&pksort_kernel<U, P, LG, NSG_PK_E, true>)      \
+                : reinterpret_cast<const void*>(&pksort_kernel<U, P, LG, NSG_PK_E, false>);
+    NSG_PK_CASE(5)
+    NSG_PK_CASE(6)
+    NSG_PK_CASE(7)
+    NSG_PK_CASE(8)
+#undef NSG_PK_CASE
+    default: return nullptr;
+  }
+}
+
+const void* pk_pick(int kb, int pay, int lognr, bool full, int* smem) {
+  if (kb == 4) {
+    if (pay == 0) return pk_fn<uint32_t, NoPay>(lognr, full, smem);
+    if (pay == 1) return pk_fn<uint32_t, uint32_t>(lognr, full, smem);
+    return pk_fn<uint32_t, uint64_t>(lognr, full, smem);
+  }
+  if (pay == 0) return pk_fn<uint64_t, NoPay>(lognr, full, smem);
+  if (pay == 1) return pk_fn<uint64_t, uint32_t>(lognr, full, smem);
+  return pk_fn<uint64_t, uint64_t>(lognr, full, smem);
+}
+
+}  // namespace
+
+bool pksort_covers(int64_t n) { return n >= 17 && n <= 256; }
+
+int launch_pksort(const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows, int64_t n,
+                  int key_bytes, int pay, const Xform& xf, cudaStream_t st) {
+  if (!pksort_covers(n)) return fail(NSG_ERR_SPEC, "packed warp sorter covers 17..256 items, got %lld", (long long)n);
+  if (rows <= 0) return 0;
+  int lognr = 5;
+  while ((1 << lognr) < n) ++lognr;
+  int smem = 0;
+  const void* fn = pk_pick(key_bytes, pay, lognr, n == (int64_t(1) << lognr), &smem);
+  if (!fn) return fail(NSG_ERR_SPEC, "no packed warp sorter for this configuration");
+  const auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  const bool bulk = al(k_in) && al(k_out) && (pay == 0 || (al(p_in) && al(p_out))) && !env_flag("NSG_PK_NOBULK");
+  PkParams prm{k_in, k_out, p_in, p_out, rows, int(n), bulk ? 1 : 0, 1u, 0xffffffffu, xf};
+  int sms = 0, occ = 0;
+  constexpr int threads = NSG_PK_WARPS * 32;
+  if (int rc = kernel_residency(fn, threads, smem, &occ, &sms)) return rc;
+  const int64_t rows_per_cta = int64_t(NSG_PK_WARPS) * ((32 * NSG_PK_E) >> lognr);
+  const int64_t need = (rows + rows_per_cta - 1) / rows_per_cta;
+  const int64_t grid = need < int64_t(sms) * occ ? need : int64_t(sms) * occ;
+  void* args[] = {&prm};
+  const cudaError_t e = cudaLaunchKernel(fn, dim3(unsigned(grid)), dim3(threads), args, size_t(smem), st);
+  if (e != cudaSuccess) return fail(NSG_ERR_CUDA, "pksort_kernel launch: %s", cudaGetErrorString(e));
+  return 0;
+}
+
+unsigned long long pksort_fallback_rows(bool reset) {
+  unsigned long long v = 0;
+  cudaMemcpyFromSymbol(&v, g_pk_fallback_rows, sizeof(v));
+  if (reset) {
+    const unsigned long long z = 0;
+    cudaMemcpyToSymbol(g_pk_fallback_rows, &z, sizeof(z));
+  }
+  return v;
+}
+
+}  // namespace nsg

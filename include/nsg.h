@@ -154,11 +154,10 @@ int nsg_scan_sorted(const void* keys, int key_bytes, int64_t stride_bytes, int64
 int nsg_fill_splitmix(void* out, int64_t count, int elem_bytes, uint64_t seed, uint64_t first_index,
                       void* stream);
 
-/* Diagnostics of the packed-key row kernels -- the level-synchronous RSS
- * kernel and the merge sorter's packed warp sorter (no reference
- * counterpart): rows they re-sorted with the exact warp sorter because the
- * 32-bit packed keys tied (or an RSS bucket overflowed) since the last
- * reset, on the current device.  reset != 0 zeroes the counter after reading it. */
+/* Diagnostics of the packed-key row kernels (csrc/pksort.cu: the RSS level
+ * and the merge sorter; no reference counterpart): rows they re-sorted with
+ * the exact warp sorter because distinct keys tied on their 32-bit packed
+ * words, since the last reset, on the current device.  reset != 0 zeroes the counter after reading it. */
 unsigned long long nsg_rss_fallback_rows(int reset);
 
 /* Last error message of the calling thread ("" if none). */

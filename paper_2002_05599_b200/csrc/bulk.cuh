@@ -1,5 +1,5 @@
 // TMA bulk-copy (cp.async.bulk) and mbarrier helpers for the warp-owned
-// staging rings of the row sorters (pksort.cu, rsslvl.cu).
+// staging rings of the row sorters (pksort.cu).
 //
 // One lane of a warp arms the buffer's mbarrier with the byte count and issues
 // the 1-D bulk copy global -> shared; the copy engine completes the

@@ -194,7 +194,7 @@ extern "C" {
 
 const char* nsg_last_error(void) { return g_err.c_str(); }
 unsigned long long nsg_rss_fallback_rows(int reset) {
-  return rsslvl_fallback_rows(reset != 0) + pksort_fallback_rows(reset != 0);
+  return pksort_fallback_rows(reset != 0);
 }
 int nsg_version(void) { return 100; }
 

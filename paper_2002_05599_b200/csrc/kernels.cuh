@@ -33,16 +33,14 @@ int launch_rss_segment_list(const nsg_spec& sp, const uint32_t* offsets, const u
                             uint32_t* overflow, int64_t max_rows, const void* keys_in, void* keys_out,
                             const void* pay_in, void* pay_out, cudaStream_t st);
 
-// rsslvl.cu (level-synchronous RSS, keys-only / UNIQUE rows of 17..256 items)
-bool rsslvl_covers(int64_t n);
-int launch_rsslvl(const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows, int64_t n,
-                  int key_bytes, int pay, uint32_t seed, const Xform& xf, cudaStream_t st);
-unsigned long long rsslvl_fallback_rows(bool reset);
-
 // pksort.cu (packed-key warp sorter: merge kind, keys-only / UNIQUE rows of 17..256 items)
 bool pksort_covers(int64_t n);
 int launch_pksort(const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows, int64_t n,
                   int key_bytes, int pay, const Xform& xf, cudaStream_t st);
+// the same skeleton with one Register Sample Sort level as the sort phase
+// (rss kind, keys-only / UNIQUE rows of 17..256 items)
+int launch_pkrss(const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows, int64_t n,
+                 int key_bytes, int pay, uint32_t seed, const Xform& xf, cudaStream_t st);
 unsigned long long pksort_fallback_rows(bool reset);
 
 // wmerge.cu

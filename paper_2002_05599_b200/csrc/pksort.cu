@@ -64,12 +64,24 @@ struct PkParams {
   int n;
   int bulk;  // TMA bulk copies allowed (16-byte aligned group chunks)
   uint32_t one, neg1;  // 1 and ~0, opaque to the compiler (PipeK)
+  uint32_t seed;       // RSS sample seed (the reference's rss_sample_seed)
   Xform xf;
 };
 
 __host__ __device__ constexpr int pk_ilog2(int x) { return x <= 1 ? 0 : 1 + pk_ilog2(x >> 1); }
 
-template <class U, class P, int LOGNR, int E>
+// the reference generator (minstd, netsort_core.c:38-40) applied j times
+__device__ __forceinline__ uint32_t lcg_jump_dev(uint32_t s, int j) {
+  constexpr uint64_t kM = 2147483647u;
+  uint64_t m = 48271u, r = 1;
+  for (int e = j; e; e >>= 1) {
+    if (e & 1) r = (r * m) % kM;
+    m = (m * m) % kM;
+  }
+  return uint32_t((uint64_t(s) * r) % kM);
+}
+
+template <class U, class P, int LOGNR, int E, int SCRATCH = 0>
 struct PkCfg {
   static constexpr bool HAS_P = !IsNoPay<P>::value;
   static constexpr int PB = PayBytes<P>::value;
@@ -85,13 +97,14 @@ struct PkCfg {
   // ring depth: one buffer being sorted, one draining its bulk store, the
   // rest (>= 1) loading ahead -- HBM latency x bandwidth per SM wants
   // ~64 KB of loads in flight, so deeper rings for smaller groups
-  static constexpr int NB_RAW = NSG_PK_RING_BYTES / (KB + PBB);
+  static constexpr int NB_RAW = (SCRATCH ? NSG_PK_RING_BYTES / 2 : NSG_PK_RING_BYTES) / (KB + PBB);
   static constexpr int NB = NB_RAW < 3 ? 3 : NB_RAW > 8 ? 8 : NB_RAW;
   static constexpr int AHEAD = NB - 2;  // groups loading ahead of the one being sorted
   static constexpr int OFF_K = 0;
   static constexpr int OFF_P = OFF_K + NB * KB;
   static constexpr int OFF_PA = OFF_P + NB * PBB;
-  static constexpr int OFF_BAR = (OFF_PA + R * S * 4 + 7) / 8 * 8;
+  static constexpr int OFF_SC = OFF_PA + R * S * 4;
+  static constexpr int OFF_BAR = (OFF_SC + SCRATCH * 4 + 7) / 8 * 8;
   static constexpr int WARP_SMEM = (OFF_BAR + NB * 8 + 127) / 128 * 128;
   static constexpr int WARPS = NSG_PK_WARPS;
   static constexpr int CTA_SMEM = WARPS * WARP_SMEM;
@@ -276,11 +289,144 @@ __device__ __noinline__ void pk_exact_row(U* rk, P* rp, int n, const Xform xf, i
   __syncwarp();
 }
 
+// ---------------------------------------------------------------------------
+// Sort phases.  Both take the row's packed words in registers -- lane ll of
+// the row's L lanes holds columns ll + L*r, r < E -- and leave them sorted in
+// the blocked layout (lane ll holds sorted positions ll*E .. ll*E+E-1).
+// ---------------------------------------------------------------------------
+struct PhaseCtx {
+  int lane, g, ll, n, rl;   // rl: valid r of this lane (E when the row is full)
+  bool rowv;
+  uint32_t* sc;             // per-warp scratch (PH::SCRATCH words)
+  uint32_t spos;            // RSS: this lane's sample column
+  PipeK k;
+};
+
+// Merge sorter: in-lane best network + bitonic merges across lanes.
+template <int LOGNR, int E>
+struct PhaseBitonic {
+  static constexpr int L = (1 << LOGNR) / E;
+  static constexpr int SCRATCH = 0;
+  __device__ __forceinline__ static unsigned sort(uint32_t (&pk)[E], const PhaseCtx& c) {
+    lane_sort<E>(pk, c.k);
+    merge_lanes32<E, L>(pk, c.ll, c.k);
+    return 0u;
+  }
+};
+
+// Register Sample Sort, one level (north star (d); reference ns_rss_rec,
+// netsort_core.c:325-391): the row's L lanes draw one sample each at the
+// reference generator's positions (minstd, netsort_core.c:38-40), sort the
+// samples across lanes into L-1 splitters held one per lane, classify every
+// word branch-free by binary search over the splitters (shuffles), count and
+// scatter into bucket order with shared-memory atomics.  Base case: the
+// bucket-ordered row is read back 8 words per lane, each lane sorts its 8
+// with the best-known 19-comparator network, and merge-split rounds between
+// neighbouring lanes (odd-even transposition of 8-word blocks) finish it.  A
+// bucket of B words spans at most ceil((B-1)/8)+1 blocks and every other
+// block pair is already in order, so that many rounds sort the row (0-1
+// principle: under any threshold only one bucket is mixed); the round count
+// follows the warp's largest bucket, so there is no overflow case.
+template <int LOGNR>
+struct PhaseRss {
+  static constexpr int E = 8;
+  static constexpr int NR = 1 << LOGNR;
+  static constexpr int L = NR / E;
+  static constexpr int LOGL = pk_ilog2(L);
+  static constexpr int R = 32 * E / NR;
+  static constexpr int SCRATCH = R * NR + 32;  // bucket array + counters
+
+  __device__ __forceinline__ static unsigned sort(uint32_t (&pk)[E], const PhaseCtx& c) {
+    uint32_t* pb = c.sc;                 // R rows x NR words: column order, then bucket order
+    uint32_t* cnt = c.sc + R * NR;       // 32 bucket counters / starts (bucket g*L + b)
+    const int lane = c.lane, g = c.g, ll = c.ll;
+    uint32_t* prow = pb + g * NR;
+#pragma unroll
+    for (int r = 0; r < E; ++r) prow[ll + L * r] = pk[r];
+    cnt[lane] = 0u;
+    __syncwarp();
+    // ---- sample + splitters ------------------------------------------------
+    uint32_t s = c.rowv ? prow[c.spos] : 0xffffffffu;
+#pragma unroll
+    for (int k2 = 2; k2 <= L; k2 <<= 1) {
+#pragma unroll
+      for (int j2 = k2 >> 1; j2 > 0; j2 >>= 1) {
+        const uint32_t o = __shfl_xor_sync(0xffffffffu, s, j2);
+        const bool up = (ll & k2) == 0;
+        const bool low = (ll & j2) == 0;
+        s = (low == up) ? min(s, o) : max(s, o);
+      }
+    }
+    // ---- classify: binary search over the row's L-1 splitters ---------------
+    int q[E];
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+      int b = g << LOGL;  // lane of the row's first bucket
+#pragma unroll
+      for (int step = L / 2; step >= 1; step >>= 1) {
+        const uint32_t t = __shfl_sync(0xffffffffu, s, b + step - 1);
+        b |= t < pk[r] ? step : 0;
+      }
+      q[r] = b;
+      if (r < c.rl) atomicAdd(&cnt[q[r]], 1u);
+    }
+    __syncwarp();
+    // ---- bucket starts (segmented scan over the row's lanes), scatter ---------
+    const uint32_t cb = cnt[lane];
+    uint32_t incl = cb;
+#pragma unroll
+    for (int d = 1; d < L; d <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
+      if (ll >= d) incl += t;
+    }
+    const uint32_t maxb = __reduce_max_sync(0xffffffffu, cb);
+    __syncwarp();
+    cnt[lane] = uint32_t(g * NR) + incl - cb;
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+      if (r < c.rl) pb[atomicAdd(&cnt[q[r]], 1u)] = pk[r];
+    }
+    __syncwarp();
+    // ---- base case: 8-word blocks, network, merge-split rounds ---------------
+#pragma unroll
+    for (int r = 0; r < E; ++r) pk[r] = prow[ll * E + r];
+    Net<0, E>::template run_k<CxAlu>(pk, c.k);
+    const int rounds = maxb <= 1u ? 0 : min(int(maxb - 2u) / E + 2, L);
+    for (int t = 0; t < rounds; ++t) {
+      // pairs (2m, 2m+1) on even rounds, (2m+1, 2m+2) on odd ones, inside the row
+      const int pl = (t & 1) ? ((ll & 1) ? ll + 1 : ll - 1) : (ll ^ 1);
+      const bool active = pl >= 0 && pl < L;
+      const bool lower = ll < pl;
+      const int src = active ? (g << LOGL) + pl : lane;
+      // an inactive lane merges with itself: min(v[r], v[7-r]) for r < 4 and
+      // max above leave its sorted block unchanged
+      const bool lo_half = !active || lower, hi_half = active && lower;
+      uint32_t o[E];
+#pragma unroll
+      for (int r = 0; r < E; ++r) o[r] = __shfl_sync(0xffffffffu, pk[E - 1 - r], src);
+#pragma unroll
+      for (int r = 0; r < E; ++r) {
+        const bool mn = r < E / 2 ? lo_half : hi_half;
+        pk[r] = mn ? min(pk[r], o[r]) : max(pk[r], o[r]);
+      }
+#pragma unroll
+      for (int j = E / 2; j > 0; j >>= 1) {
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          if ((r & j) == 0) CxAlu::cx(pk[r], pk[r | j], c.k);
+        }
+      }
+    }
+    return 0u;
+  }
+};
+
 // FULL: n == NR (no padding slots) -- the validity tests drop out; rows past
 // the end of the batch in the last group are sorted as garbage, never stored.
-template <class U, class P, int LOGNR, int E, bool FULL>
+template <class U, class P, int LOGNR, int E, bool FULL, class PH>
 __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParams prm) {
-  using C = PkCfg<U, P, LOGNR, E>;
+  using C = PkCfg<U, P, LOGNR, E, PH::SCRATCH>;
   constexpr int NR = C::NR, R = C::R, L = C::L, LOGL = C::LOGL, W = C::W, S = C::S, NB = C::NB;
   constexpr bool HAS_P = C::HAS_P;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -291,6 +437,7 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
   P* pbuf = reinterpret_cast<P*>(wsm + C::OFF_P);
   uint32_t* pa = reinterpret_cast<uint32_t*>(wsm + C::OFF_PA);
   uint64_t* bar = reinterpret_cast<uint64_t*>(wsm + C::OFF_BAR);
+  uint32_t* scratch = reinterpret_cast<uint32_t*>(wsm + C::OFF_SC);
   const U* kin = static_cast<const U*>(prm.k_in);
   const P* pin = static_cast<const P*>(prm.p_in);
   U* kout = static_cast<U*>(prm.k_out);
@@ -304,6 +451,8 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
   const int64_t groups = (rows + R - 1) / R;
   const int64_t gw = int64_t(blockIdx.x) * C::WARPS + warp;
   const int64_t GW = int64_t(gridDim.x) * C::WARPS;
+  // RSS: lane ll samples column lcg^(ll+1)(seed) mod n of its row
+  const uint32_t spos = PH::SCRATCH ? lcg_jump_dev(prm.seed, ll + 1) % uint32_t(n) : 0u;
 
   if (lane == 0) {
 #pragma unroll
@@ -415,9 +564,12 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
       }
     }
 
-    // ---- 2. sort: in-lane network + bitonic merges across the row's lanes ----
-    lane_sort<E>(pk, kk);
-    merge_lanes32<E, L>(pk, ll, kk);
+    // ---- 2. sort (bitonic merges or one RSS level) --------------------------
+    unsigned forced;
+    {
+      const PhaseCtx pc{lane, g, ll, n, rl, rowv, scratch, spos, kk};
+      forced = PH::sort(pk, pc);
+    }
 
     // ---- 3. sorted neighbours with equal packed prefixes? ---------------------
     bool tied;
@@ -428,12 +580,11 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
       for (int r = 0; r + 1 < E; ++r) eq |= (FULL || r + 1 < lim) && ((pk[r] ^ pk[r + 1]) >> LOGNR) == 0u;
       const uint32_t prev = __shfl_up_sync(0xffffffffu, pk[E - 1], 1);
       eq |= ll > 0 && (FULL || lim > 0) && ((prev ^ pk[0]) >> LOGNR) == 0u;
-      tied = __ballot_sync(0xffffffffu, eq) != 0u;
+      tied = forced == 0u && __ballot_sync(0xffffffffu, eq) != 0u;
     }
 
     // ---- 4. transpose blocked -> striped, gather the full items --------------
-    // sorted position q = ll + L*r sits at pr[q + q/E] (one pad word per E);
-    // q/E = (L*r)/E because ll < L <= E
+    // sorted position q = ll + L*r sits at pr[q + q/E] (one pad word per E)
     uint32_t* pr = pa + g * S;
 #pragma unroll
     for (int r = 0; r < E; ++r) pr[ll * (E + 1) + r] = pk[r];
@@ -443,7 +594,8 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
 #pragma unroll
     for (int r = 0; r < E; ++r) {
       if (FULL || r < rl) {
-        const uint32_t idx = pr[ll + L * r + (L * r) / E] & uint32_t(NR - 1);
+        const int q = ll + L * r;  // q / E folds to (L*r)/E when L <= E
+        const uint32_t idx = pr[L <= E ? q + (L * r) / E : q + q / E] & uint32_t(NR - 1);
         ok[r] = rk[idx];
         if constexpr (HAS_P) op[r] = rp[idx];
       }
@@ -461,7 +613,7 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
     // ---- 5. rows with packed ties: full (key, payload) order check of every
     //         sorted neighbour pair in the staged output; failures re-sorted
     //         exactly (rare: distinct keys agreeing on every kept bit) ---------
-    unsigned bad_rows = 0;
+    unsigned bad_rows = forced & ((rin >= 32 ? 0u : (1u << rin)) - 1u);
     if (tied) {
       const U M = U(xf.sign_or ^ xf.kdesc);
       auto kord = [&](U v) -> U { return xf.flt ? to_ord<U>(v, xf) : U(v ^ M); };
@@ -513,14 +665,27 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
   if (lane == 0) bulk_wait<0>();
 }
 
+template <class U, class P, int LG, bool RSS>
+const void* pk_fn_lg(bool full, int* smem) {
+  if constexpr (RSS) {
+    using PH = PhaseRss<LG>;
+    *smem = PkCfg<U, P, LG, PH::E, PH::SCRATCH>::CTA_SMEM;
+    return full ? reinterpret_cast<const void*>(&pksort_kernel<U, P, LG, PH::E, true, PH>)
+                : reinterpret_cast<const void*>(&pksort_kernel<U, P, LG, PH::E, false, PH>);
+  } else {
+    using PH = PhaseBitonic<LG, NSG_PK_E>;
+    *smem = PkCfg<U, P, LG, NSG_PK_E, 0>::CTA_SMEM;
+    return full ? reinterpret_cast<const void*>(&pksort_kernel<U, P, LG, NSG_PK_E, true, PH>)
+                : reinterpret_cast<const void*>(&pksort_kernel<U, P, LG, NSG_PK_E, false, PH>);
+  }
+}
+
 template <class U, class P>
-const void* pk_fn(int lognr, bool full, int* smem) {
+const void* pk_fn(int lognr, bool full, bool rss, int* smem) {
   switch (lognr) {
-#define NSG_PK_CASE(LG)                                                                        \
-  case LG:                                                                                     \
-    *smem = PkCfg<U, P, LG, NSG_PK_E>::CTA_SMEM;                                               \
-    return full ? reinterpret_cast<const void*>(&pksort_kernel<U, P, LG, NSG_PK_E, true>)      \
-                : reinterpret_cast<const void*>(&pksort_kernel<U, P, LG, NSG_PK_E, false>);
+#define NSG_PK_CASE(LG)                                                                       \
+  case LG:                                                                                    \
+    return rss ? pk_fn_lg<U, P, LG, true>(full, smem) : pk_fn_lg<U, P, LG, false>(full, smem);
     NSG_PK_CASE(5)
     NSG_PK_CASE(6)
     NSG_PK_CASE(7)
@@ -530,43 +695,54 @@ const void* pk_fn(int lognr, bool full, int* smem) {
   }
 }
 
-const void* pk_pick(int kb, int pay, int lognr, bool full, int* smem) {
+const void* pk_pick(int kb, int pay, int lognr, bool full, bool rss, int* smem) {
   if (kb == 4) {
-    if (pay == 0) return pk_fn<uint32_t, NoPay>(lognr, full, smem);
-    if (pay == 1) return pk_fn<uint32_t, uint32_t>(lognr, full, smem);
-    return pk_fn<uint32_t, uint64_t>(lognr, full, smem);
+    if (pay == 0) return pk_fn<uint32_t, NoPay>(lognr, full, rss, smem);
+    if (pay == 1) return pk_fn<uint32_t, uint32_t>(lognr, full, rss, smem);
+    return pk_fn<uint32_t, uint64_t>(lognr, full, rss, smem);
   }
-  if (pay == 0) return pk_fn<uint64_t, NoPay>(lognr, full, smem);
-  if (pay == 1) return pk_fn<uint64_t, uint32_t>(lognr, full, smem);
-  return pk_fn<uint64_t, uint64_t>(lognr, full, smem);
+  if (pay == 0) return pk_fn<uint64_t, NoPay>(lognr, full, rss, smem);
+  if (pay == 1) return pk_fn<uint64_t, uint32_t>(lognr, full, rss, smem);
+  return pk_fn<uint64_t, uint64_t>(lognr, full, rss, smem);
 }
 
 }  // namespace
 
 bool pksort_covers(int64_t n) { return n >= 17 && n <= 256; }
 
-int launch_pksort(const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows, int64_t n,
-                  int key_bytes, int pay, const Xform& xf, cudaStream_t st) {
-  if (!pksort_covers(n)) return fail(NSG_ERR_SPEC, "packed warp sorter covers 17..256 items, got %lld", (long long)n);
+static int launch_pk(const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows, int64_t n,
+                     int key_bytes, int pay, const Xform& xf, bool rss, uint32_t seed, cudaStream_t st) {
+  if (!pksort_covers(n)) return fail(NSG_ERR_SPEC, "packed warp sorters cover 17..256 items, got %lld", (long long)n);
   if (rows <= 0) return 0;
   int lognr = 5;
   while ((1 << lognr) < n) ++lognr;
   int smem = 0;
-  const void* fn = pk_pick(key_bytes, pay, lognr, n == (int64_t(1) << lognr), &smem);
+  const void* fn = pk_pick(key_bytes, pay, lognr, n == (int64_t(1) << lognr), rss, &smem);
   if (!fn) return fail(NSG_ERR_SPEC, "no packed warp sorter for this configuration");
   const auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   const bool bulk = al(k_in) && al(k_out) && (pay == 0 || (al(p_in) && al(p_out))) && !env_flag("NSG_PK_NOBULK");
-  PkParams prm{k_in, k_out, p_in, p_out, rows, int(n), bulk ? 1 : 0, 1u, 0xffffffffu, xf};
+  PkParams prm{k_in, k_out, p_in, p_out, rows, int(n), bulk ? 1 : 0, 1u, 0xffffffffu, seed == 0 ? 1u : seed, xf};
   int sms = 0, occ = 0;
   constexpr int threads = NSG_PK_WARPS * 32;
   if (int rc = kernel_residency(fn, threads, smem, &occ, &sms)) return rc;
-  const int64_t rows_per_cta = int64_t(NSG_PK_WARPS) * ((32 * NSG_PK_E) >> lognr);
+  const int e = rss ? PhaseRss<5>::E : NSG_PK_E;
+  const int64_t rows_per_cta = int64_t(NSG_PK_WARPS) * ((32 * e) >> lognr);
   const int64_t need = (rows + rows_per_cta - 1) / rows_per_cta;
   const int64_t grid = need < int64_t(sms) * occ ? need : int64_t(sms) * occ;
   void* args[] = {&prm};
-  const cudaError_t e = cudaLaunchKernel(fn, dim3(unsigned(grid)), dim3(threads), args, size_t(smem), st);
-  if (e != cudaSuccess) return fail(NSG_ERR_CUDA, "pksort_kernel launch: %s", cudaGetErrorString(e));
+  const cudaError_t err = cudaLaunchKernel(fn, dim3(unsigned(grid)), dim3(threads), args, size_t(smem), st);
+  if (err != cudaSuccess) return fail(NSG_ERR_CUDA, "pksort_kernel launch: %s", cudaGetErrorString(err));
   return 0;
+}
+
+int launch_pksort(const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows, int64_t n,
+                  int key_bytes, int pay, const Xform& xf, cudaStream_t st) {
+  return launch_pk(k_in, k_out, p_in, p_out, rows, n, key_bytes, pay, xf, false, 0u, st);
+}
+
+int launch_pkrss(const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows, int64_t n,
+                 int key_bytes, int pay, uint32_t seed, const Xform& xf, cudaStream_t st) {
+  return launch_pk(k_in, k_out, p_in, p_out, rows, n, key_bytes, pay, xf, true, seed, st);
 }
 
 unsigned long long pksort_fallback_rows(bool reset) {

@@ -1003,12 +1003,12 @@ int launch_rss(const nsg_spec& sp, const void* k_in, void* k_out, const void* p_
       return fail(NSG_ERR_SPEC, "network base case caps the threshold at 16");
   }
   // keys-only / UNIQUE rows: the output is the unique sorted order, so the
-  // level-synchronous kernel (rsslvl.cu) serves them; the draw-for-draw
+  // packed-key warp kernel with one RSS level (pksort.cu) serves them; the draw-for-draw
   // kernels below stay for REF mode (payload order under key ties), AoS
   // items, CSR segment lists and NSG_RSS_FAITHFUL=1.
   if (sp.kind == NSG_KIND_RSS && layout == LAYOUT_SOA && !seg_ids && (pay == 0 || mode == MODE_UNIQUE) &&
-      rsslvl_covers(n) && !env_flag_set("NSG_RSS_FAITHFUL"))
-    return launch_rsslvl(k_in, k_out, p_in, p_out, rows, n, key_bytes, pay, sp.rss_sample_seed, xf, st);
+      pksort_covers(n) && !env_flag_set("NSG_RSS_FAITHFUL"))
+    return launch_pkrss(k_in, k_out, p_in, p_out, rows, n, key_bytes, pay, sp.rss_sample_seed, xf, st);
   RssParams prm{};
   prm.k_in = k_in;
   prm.k_out = k_out;

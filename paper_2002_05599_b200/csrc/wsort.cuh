@@ -1,6 +1,6 @@
 // Warp-cooperative bitonic sort building blocks shared by the merge sorter
 // (wmerge.cu) and the level-synchronous RSS kernel's exact fallback
-// (rsslvl.cu): E items per lane in a BLOCKED layout (lane l holds positions
+// (pksort.cu): E items per lane in a BLOCKED layout (lane l holds positions
 // l*E .. l*E+E-1); stages with partner distance < E are in-register
 // compare-exchanges, the others exchange with lane l ^ (j/E) by shuffle.
 #pragma once

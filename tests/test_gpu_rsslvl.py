@@ -1,4 +1,4 @@
-"""GPU parity of the level-synchronous RSS kernel (csrc/rsslvl.cu) -- the
+"""GPU parity of the packed-key RSS kernel (csrc/pksort.cu, PhaseRss) -- the
 keys-only / UNIQUE path of `kind="rss"` for 17..256 items -- against the
 oracle (reference restatement) and np.sort, including the inputs that force
 its exact fallback (packed-key ties) and the reference RSS tests' shapes

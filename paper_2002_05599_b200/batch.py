@@ -172,9 +172,11 @@ def sort_segments(offsets, keys, payload=None, *, family: str = "best", swap: st
                   workspace=None, check: bool = True):
     """Sort CSR segments [offsets[s], offsets[s+1]) of keys (+payload), on device.
 
-    Segments of up to 1024 items are supported; with `check` (default) the
-    call synchronises and raises ConfigurationError if a longer one was
-    present (it is left unsorted).  `check=False` keeps the call fully
+    Keys-only and UNIQUE segments of any length up to the CTA sorter's
+    shared-memory capacity (8192 16-byte / 16384 8-byte / 32768 4-byte items)
+    are sorted; REF mode with a payload covers up to 1024 items.  With `check`
+    (default) the call synchronises and raises ConfigurationError if a longer
+    one was present (it is left unsorted).  `check=False` keeps the call fully
     asynchronous for callers that bound their segment lengths."""
     import torch
     if not _is_torch(keys) or not keys.is_cuda:

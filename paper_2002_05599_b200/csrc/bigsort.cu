@@ -1,0 +1,360 @@
+// Rows and CSR segments longer than the warp sorters' 1024 items (SURVEY
+// 8(f)4; the reference's ns_rss_rec, netsort_core.c:325-391, has no size cap,
+// and its hybrid sorts hand large arrays to the same recursion,
+// hybridsort.py:45-49).
+//
+// Keys-only and UNIQUE (key, payload) order only: the output order is unique,
+// so any exact sorter reproduces the reference bit for bit.  One CTA of 1024
+// threads owns one row / segment at a time:
+//
+//  * len <= CAP (the largest power of two whose keys + payloads fit in
+//    ~128 KB of shared memory: 8192 16-byte items, 16384 8-byte, 32768 4-byte):
+//    the row is staged in shared memory in the order-preserving space, padded
+//    with +inf to a power of two, bitonic-sorted there (all compare-exchanges
+//    of a stage in parallel, one CTA barrier per stage) and written back;
+//  * len > CAP (rows only, with a caller-provided scratch of the same size):
+//    CAP-item tiles are sorted as above, then merge passes double the sorted
+//    run length -- each thread finds its merge-path split of the output range
+//    by binary search and merges 8 outputs -- ping-ponging between the output
+//    and the scratch so that the last pass lands in the output.
+//
+// Segment lists: the entries come from the CSR front end's long-segment list
+// (segments.cu); this kernel takes the ones above 1024 items (the warp RSS
+// kernel takes the rest) and counts those above CAP as overflow.
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace nsg {
+
+namespace {
+
+constexpr int kBigThreads = 1024;
+constexpr int kBigSmemBudget = 128 * 1024;
+constexpr int kMergePer = 8;  // outputs per thread per merge step
+
+struct BigParams {
+  const void* k_in;
+  void* k_out;
+  const void* p_in;
+  void* p_out;
+  void* k_scr;  // scratch (len > CAP rows), may be null
+  void* p_scr;
+  int64_t items;  // rows, or capacity of the segment list
+  int64_t n;      // row length (rows mode)
+  const uint32_t* seg_off;
+  const uint32_t* seg_ids;
+  const uint32_t* seg_count;
+  uint32_t* overflow;
+  int64_t min_len;  // segment lists: only entries longer than this
+  Xform xf;
+};
+
+template <class U, class P>
+struct BigCfg {
+  static constexpr int EB = int(sizeof(U)) + PayBytes<P>::value;
+  static constexpr int CAP = EB <= 4 ? 32768 : EB <= 8 ? 16384 : 8192;
+  static_assert(CAP * EB <= kBigSmemBudget, "smem budget");
+  static constexpr int SMEM = CAP * EB;
+};
+
+template <class U, class P>
+__device__ __forceinline__ bool big_lt(U bk, const P& bp, U ak, const P& ap) {
+  if constexpr (IsNoPay<P>::value) {
+    return key_lt(bk, ak);
+  } else {
+    return lex_lt(bk, bp, ak, ap);
+  }
+}
+
+template <class U, class P>
+__device__ __forceinline__ U ord_k(U k, const Xform& xf) { return xf.active ? to_ord<U>(k, xf) : k; }
+template <class U, class P>
+__device__ __forceinline__ U unord_k(U k, const Xform& xf) { return xf.active ? from_ord<U>(k, xf) : k; }
+template <class P>
+__device__ __forceinline__ P xp(P q, const Xform& xf) {
+  if constexpr (IsNoPay<P>::value) {
+    return q;
+  } else {
+    return xf.active ? P(q ^ P(xf.pdesc)) : q;
+  }
+}
+
+// Sort `len` (<= CAP) items of src into dst through shared memory.  `ord_in`:
+// src already holds order-preserving keys; `ord_out`: leave dst in that space.
+template <class U, class P>
+__device__ void smem_sort(const U* ksrc, const P* psrc, U* kdst, P* pdst, int len, bool ord_in, bool ord_out,
+                          const Xform& xf, unsigned char* smem) {
+  using C = BigCfg<U, P>;
+  constexpr bool HAS_P = !IsNoPay<P>::value;
+  U* sk = reinterpret_cast<U*>(smem);
+  P* sp = reinterpret_cast<P*>(smem + C::CAP * sizeof(U));
+  int np = 2;
+  while (np < len) np <<= 1;
+  for (int i = threadIdx.x; i < np; i += kBigThreads) {
+    if (i < len) {
+      sk[i] = ord_in ? ksrc[i] : ord_k<U, P>(ksrc[i], xf);
+      if constexpr (HAS_P) sp[i] = ord_in ? psrc[i] : xp<P>(psrc[i], xf);
+    } else {
+      sk[i] = U(~U(0));
+      if constexpr (HAS_P) sp[i] = P(~P(0));
+    }
+  }
+  __syncthreads();
+  const int half = np >> 1;
+  for (int k = 2; k <= np; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = threadIdx.x; t < half; t += kBigThreads) {
+        const int i = 2 * t - (t & (j - 1));  // low index of the pair (bit j clear)
+        const int m = i + j;
+        const bool asc = (i & k) == 0;
+        const U ki = sk[i], km = sk[m];
+        P pi{}, pm{};
+        if constexpr (HAS_P) {
+          pi = sp[i];
+          pm = sp[m];
+        }
+        const bool sw = big_lt<U, P>(km, pm, ki, pi) == asc;
+        if (sw) {
+          sk[i] = km;
+          sk[m] = ki;
+          if constexpr (HAS_P) {
+            sp[i] = pm;
+            sp[m] = pi;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < len; i += kBigThreads) {
+    kdst[i] = ord_out ? sk[i] : unord_k<U, P>(sk[i], xf);
+    if constexpr (HAS_P) pdst[i] = ord_out ? sp[i] : xp<P>(sp[i], xf);
+  }
+  __syncthreads();
+}
+
+// items of merge(A[0..na), B[0..nb)) among its first d outputs that come
+// from A (A first on ties)
+template <class U, class P>
+__device__ __forceinline__ int64_t merge_split(const U* ak, const P* ap, int64_t na, const U* bk, const P* bp,
+                                               int64_t nb, int64_t d) {
+  constexpr bool HAS_P = !IsNoPay<P>::value;
+  int64_t lo = d > nb ? d - nb : 0, hi = d < na ? d : na;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    P pa{}, pb{};
+    if constexpr (HAS_P) {
+      pa = ap[mid];
+      pb = bp[d - 1 - mid];
+    }
+    if (!big_lt<U, P>(bk[d - 1 - mid], pb, ak[mid], pa))
+      lo = mid + 1;  // A[mid] <= B[d-1-mid]: A[mid] is among the first d
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// One merge pass over a row of `len` ord-space items: runs of `w` from src
+// merged pairwise into dst (the CTA walks the row in chunks).
+template <class U, class P>
+__device__ void merge_pass(const U* sk, const P* sp, U* dk, P* dp, int64_t len, int64_t w, bool last,
+                           const Xform& xf) {
+  constexpr bool HAS_P = !IsNoPay<P>::value;
+  constexpr int64_t CH = int64_t(kBigThreads) * kMergePer;
+  for (int64_t c0 = 0; c0 < len; c0 += CH) {
+    const int64_t o = c0 + int64_t(threadIdx.x) * kMergePer;  // this thread's first output
+    if (o < len) {
+      const int64_t r0 = o / (2 * w) * (2 * w);  // its run pair
+      const int64_t na = (r0 + w < len ? r0 + w : len) - r0;
+      const int64_t nb = (r0 + 2 * w < len ? r0 + 2 * w : len) - (r0 + na);
+      const U* ak = sk + r0;
+      const U* bk = sk + r0 + na;
+      const P* ap = HAS_P ? sp + r0 : sp;
+      const P* bp = HAS_P ? sp + r0 + na : sp;
+      const int64_t d = o - r0;
+      int64_t ai = merge_split<U, P>(ak, ap, na, bk, bp, nb, d);
+      int64_t bi = d - ai;
+      for (int q = 0; q < kMergePer && o + q < r0 + na + nb; ++q) {
+        bool take_a;
+        if (ai >= na) {
+          take_a = false;
+        } else if (bi >= nb) {
+          take_a = true;
+        } else {
+          P pa{}, pb{};
+          if constexpr (HAS_P) {
+            pa = ap[ai];
+            pb = bp[bi];
+          }
+          take_a = !big_lt<U, P>(bk[bi], pb, ak[ai], pa);
+        }
+        U k;
+        P p{};
+        if (take_a) {
+          k = ak[ai];
+          if constexpr (HAS_P) p = ap[ai];
+          ++ai;
+        } else {
+          k = bk[bi];
+          if constexpr (HAS_P) p = bp[bi];
+          ++bi;
+        }
+        dk[o + q] = last ? unord_k<U, P>(k, xf) : k;
+        if constexpr (HAS_P) dp[o + q] = last ? xp<P>(p, xf) : p;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+template <class U, class P>
+__global__ void __launch_bounds__(kBigThreads, 1) bigsort_kernel(const BigParams prm) {
+  using C = BigCfg<U, P>;
+  constexpr bool HAS_P = !IsNoPay<P>::value;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const U* kin = static_cast<const U*>(prm.k_in);
+  const P* pin = static_cast<const P*>(prm.p_in);
+  U* kout = static_cast<U*>(prm.k_out);
+  P* pout = static_cast<P*>(prm.p_out);
+  U* kscr = static_cast<U*>(prm.k_scr);
+  P* pscr = static_cast<P*>(prm.p_scr);
+  const Xform xf = prm.xf;
+  const int64_t items = prm.seg_ids ? min(int64_t(*prm.seg_count), prm.items) : prm.items;
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    int64_t base, len;
+    if (prm.seg_ids) {
+      const uint32_t s = prm.seg_ids[it];
+      base = prm.seg_off[s];
+      len = int64_t(prm.seg_off[s + 1]) - base;
+      if (len <= prm.min_len) continue;
+    } else {
+      base = it * prm.n;
+      len = prm.n;
+    }
+    const U* ki = kin + base;
+    const P* pi = HAS_P ? pin + base : pin;
+    U* ko = kout + base;
+    P* po = HAS_P ? pout + base : pout;
+    if (len <= C::CAP) {
+      smem_sort<U, P>(ki, pi, ko, po, int(len), false, false, xf, smem);
+      continue;
+    }
+    if (!kscr) {  // no scratch: left unsorted, counted
+      if (threadIdx.x == 0) atomicAdd(prm.overflow, 1u);
+      continue;
+    }
+    // tile sort, then merge passes; the last pass must land in the output
+    int passes = 0;
+    for (int64_t w = C::CAP; w < len; w <<= 1) ++passes;
+    U* ks = kscr + base;
+    P* ps = HAS_P ? pscr + base : pscr;
+    U* k0 = (passes & 1) ? ks : ko;  // tile-sort destination (ord space)
+    P* p0 = (passes & 1) ? ps : po;
+    for (int64_t t0 = 0; t0 < len; t0 += C::CAP) {
+      const int tl = int(len - t0 < C::CAP ? len - t0 : C::CAP);
+      smem_sort<U, P>(ki + t0, HAS_P ? pi + t0 : pi, k0 + t0, HAS_P ? p0 + t0 : p0, tl, false, true, xf, smem);
+    }
+    U* sk = k0;
+    P* sp = p0;
+    int pass = 0;
+    for (int64_t w = C::CAP; w < len; w <<= 1, ++pass) {
+      U* dk = sk == ko ? ks : ko;
+      P* dp = sk == ko ? ps : po;
+      merge_pass<U, P>(sk, sp, dk, dp, len, w, pass + 1 == passes, xf);
+      sk = dk;
+      sp = dp;
+    }
+  }
+}
+
+template <class U, class P>
+const void* big_fn(int* smem, int* cap) {
+  *smem = BigCfg<U, P>::SMEM;
+  *cap = BigCfg<U, P>::CAP;
+  return reinterpret_cast<const void*>(&bigsort_kernel<U, P>);
+}
+
+const void* big_pick(int kb, int pay, int* smem, int* cap) {
+  if (kb == 4) {
+    if (pay == 0) return big_fn<uint32_t, NoPay>(smem, cap);
+    if (pay == 1) return big_fn<uint32_t, uint32_t>(smem, cap);
+    return big_fn<uint32_t, uint64_t>(smem, cap);
+  }
+  if (pay == 0) return big_fn<uint64_t, NoPay>(smem, cap);
+  if (pay == 1) return big_fn<uint64_t, uint32_t>(smem, cap);
+  return big_fn<uint64_t, uint64_t>(smem, cap);
+}
+
+int launch_big(const BigParams& prm0, int kb, int pay, int64_t grid_items, cudaStream_t st) {
+  int smem = 0, cap = 0;
+  const void* fn = big_pick(kb, pay, &smem, &cap);
+  int sms = 0, occ = 0;
+  if (int rc = kernel_residency(fn, kBigThreads, smem, &occ, &sms)) return rc;
+  const int64_t grid = grid_items < int64_t(sms) * occ ? grid_items : int64_t(sms) * occ;
+  if (grid <= 0) return 0;
+  BigParams prm = prm0;
+  void* args[] = {&prm};
+  const cudaError_t e = cudaLaunchKernel(fn, dim3(unsigned(grid)), dim3(kBigThreads), args, size_t(smem), st);
+  if (e != cudaSuccess) return fail(NSG_ERR_CUDA, "bigsort_kernel launch: %s", cudaGetErrorString(e));
+  return 0;
+}
+
+}  // namespace
+
+int64_t bigsort_cap(int key_bytes, int pay) {
+  int smem = 0, cap = 0;
+  big_pick(key_bytes, pay, &smem, &cap);
+  return cap;
+}
+
+int launch_bigsort_rows(const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows, int64_t n,
+                        int key_bytes, int pay, const Xform& xf, cudaStream_t st) {
+  if (rows <= 0 || n <= 0) return 0;
+  const int pb = pay == 0 ? 0 : pay == 1 ? 4 : 8;
+  const int64_t cap = bigsort_cap(key_bytes, pay);
+  BigParams prm{k_in, k_out, p_in, p_out, nullptr, nullptr, rows, n, nullptr, nullptr, nullptr, nullptr, 0, xf};
+  if (n <= cap) return launch_big(prm, key_bytes, pay, rows, st);
+  // rows above CAP need a scratch copy for the merge passes: stream-ordered
+  // allocation, in batches of at most 1 GiB of scratch
+  const int64_t row_bytes = n * (key_bytes + pb);
+  int64_t batch = (int64_t(1) << 30) / row_bytes;
+  if (batch < 1) batch = 1;
+  if (batch > rows) batch = rows;
+  void* scr = nullptr;
+  cudaError_t e = cudaMallocAsync(&scr, size_t(batch * row_bytes), st);
+  if (e != cudaSuccess) return fail(NSG_ERR_CUDA, "scratch allocation (%lld bytes): %s",
+                                    (long long)(batch * row_bytes), cudaGetErrorString(e));
+  int rc = 0;
+  for (int64_t r0 = 0; r0 < rows && rc == 0; r0 += batch) {
+    const int64_t nr = rows - r0 < batch ? rows - r0 : batch;
+    const int64_t off = r0 * n;
+    BigParams b = prm;
+    b.k_in = static_cast<const unsigned char*>(k_in) + off * key_bytes;
+    b.k_out = static_cast<unsigned char*>(k_out) + off * key_bytes;
+    if (pay) {
+      b.p_in = static_cast<const unsigned char*>(p_in) + off * pb;
+      b.p_out = static_cast<unsigned char*>(p_out) + off * pb;
+    }
+    // scratch rows shifted so that `scratch + base` addresses row r (base = r * n)
+    b.k_scr = scr;
+    b.p_scr = pay ? static_cast<unsigned char*>(scr) + batch * n * key_bytes : nullptr;
+    b.items = nr;
+    rc = launch_big(b, key_bytes, pay, nr, st);
+  }
+  cudaFreeAsync(scr, st);
+  return rc;
+}
+
+int launch_bigsort_segment_list(const uint32_t* offsets, const uint32_t* ids, const uint32_t* count,
+                                uint32_t* overflow, int64_t max_items, int64_t min_len, const void* k_in, void* k_out,
+                                const void* p_in, void* p_out, int key_bytes, int pay, const Xform& xf,
+                                cudaStream_t st) {
+  if (max_items <= 0) return 0;
+  BigParams prm{k_in, k_out, p_in, p_out, nullptr, nullptr, max_items, 0, offsets, ids, count, overflow, min_len, xf};
+  return launch_big(prm, key_bytes, pay, max_items, st);
+}
+
+}  // namespace nsg

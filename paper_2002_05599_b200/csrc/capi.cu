@@ -240,6 +240,8 @@ int nsg_sort_rows(const nsg_spec* sp, const void* keys_in, void* keys_out, const
       NetParams prm{keys_in, keys_out, pay_in, pay_out, rows * g, make_xform(*sp)};
       return launch_net(mk, prm, st);
     }
+    if (n > 1024)  // CTA bitonic in shared memory, merge passes above its capacity
+      return launch_bigsort_rows(keys_in, keys_out, pay_in, pay_out, rows, n, kb, sp->payload_dtype, make_xform(*sp), st);
     return launch_wmerge(*sp, keys_in, keys_out, pay_in, pay_out, rows, n, st);  // any other n: padded
   }
   return fail(NSG_ERR_SPEC, "sorter kind %d is not a batched small-set sorter (out of scope)", sp->kind);
@@ -497,12 +499,15 @@ int nsg_sort_segments(const nsg_spec* sp, const uint32_t* offsets, int64_t nseg,
 int nsg_segments_check(const void* ws, void* stream) {
   g_err.clear();
   if (!ws) return fail(NSG_ERR_SPEC, "segments_check needs the workspace of nsg_sort_segments");
-  uint32_t words[2] = {0, 0};  // [long segment count, segments > 1024 left unsorted]
+  uint32_t words[2] = {0, 0};  // [long segment count, segments above the device limit left unsorted]
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   NSG_CUDA(cudaMemcpyAsync(words, ws, sizeof(words), cudaMemcpyDeviceToHost, st));
   NSG_CUDA(cudaStreamSynchronize(st));
   if (words[1])
-    return fail(NSG_ERR_SPEC, "%u segment(s) longer than 1024 items were left unsorted (device limit)", words[1]);
+    return fail(NSG_ERR_SPEC,
+                "%u segment(s) above the device limit were left unsorted (REF mode with a payload: 1024 items; "
+                "keys-only / UNIQUE: the CTA sorter's shared-memory capacity)",
+                words[1]);
   return 0;
 }
 

@@ -43,6 +43,15 @@ int launch_pkrss(const void* k_in, void* k_out, const void* p_in, void* p_out, i
                  int key_bytes, int pay, uint32_t seed, const Xform& xf, cudaStream_t st);
 unsigned long long pksort_fallback_rows(bool reset);
 
+// bigsort.cu (rows / segments above 1024 items, keys-only / UNIQUE)
+int64_t bigsort_cap(int key_bytes, int pay);
+int launch_bigsort_rows(const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows, int64_t n,
+                        int key_bytes, int pay, const Xform& xf, cudaStream_t st);
+int launch_bigsort_segment_list(const uint32_t* offsets, const uint32_t* ids, const uint32_t* count,
+                                uint32_t* overflow, int64_t max_items, int64_t min_len, const void* k_in, void* k_out,
+                                const void* p_in, void* p_out, int key_bytes, int pay, const Xform& xf,
+                                cudaStream_t st);
+
 // wmerge.cu
 int launch_wmerge(const nsg_spec& sp, const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows,
                   int64_t n, cudaStream_t st);

@@ -86,6 +86,7 @@ struct RssParams {
   const uint32_t* seg_off;
   const uint32_t* seg_count;
   uint32_t* seg_overflow;
+  int big_elsewhere;  // segments above NMAX are sorted by bigsort.cu: skip, do not count
 };
 
 // range / leaf descriptor: lo:11 | cnt:11 | depth:7 | buf:1 | leaf kind:2
@@ -229,8 +230,8 @@ __global__ void __launch_bounds__(RssCfg<U, P, NMAX, DAG, MODE, LAYOUT>::WARPS *
       const uint32_t s = prm.seg_ids[row];
       base = prm.seg_off[s];
       n = int(prm.seg_off[s + 1] - prm.seg_off[s]);
-      if (n > NMAX) {  // longer than the per-warp buffers: counted, left unsorted
-        if (lane == 0) atomicAdd(prm.seg_overflow, 1u);
+      if (n > NMAX) {  // longer than the per-warp buffers: bigsort.cu's, or counted and left unsorted
+        if (lane == 0 && !prm.big_elsewhere) atomicAdd(prm.seg_overflow, 1u);
         continue;
       }
     }
@@ -994,7 +995,14 @@ int launch_rss(const nsg_spec& sp, const void* k_in, void* k_out, const void* p_
                int64_t n, int key_bytes, int pay, int mode, int layout, const Xform& xf, cudaStream_t st,
                const uint32_t* seg_ids = nullptr, const uint32_t* seg_off = nullptr,
                const uint32_t* seg_count = nullptr, uint32_t* seg_overflow = nullptr) {
-  if (n > 1024) return fail(NSG_ERR_SPEC, "RSS rows are limited to 1024 items on the device, got %lld", (long long)n);
+  if (n > 1024 && !seg_ids) {
+    // keys-only / UNIQUE rows: the output is the unique sorted order -- CTA
+    // sorter (bigsort.cu); REF-mode payload order above 1024 is not replayed
+    if (layout == LAYOUT_SOA && (pay == 0 || mode == MODE_UNIQUE))
+      return launch_bigsort_rows(k_in, k_out, p_in, p_out, rows, n, key_bytes, pay, xf, st);
+    return fail(NSG_ERR_SPEC, "RSS with reference tie order (REF mode, payload) is limited to 1024 items on the "
+                "device, got %lld", (long long)n);
+  }
   if (sp.kind == NSG_KIND_RSS) {
     if (sp.rss_oversampling < 1 || sp.rss_oversampling > 16)
       return fail(NSG_ERR_SPEC, "RSS oversampling %d not in 1..16", sp.rss_oversampling);
@@ -1031,6 +1039,7 @@ int launch_rss(const nsg_spec& sp, const void* k_in, void* k_out, const void* p_
   prm.seg_off = seg_off;
   prm.seg_count = seg_count;
   prm.seg_overflow = seg_overflow;
+  prm.big_elsewhere = seg_ids && (pay == 0 || mode == MODE_UNIQUE);
   const bool per_thread = !seg_ids && n <= 32 && !env_flag_set("NSG_RSS_WARP_ONLY");
   const RssKernel k = per_thread ? rss_thread_pick(sp.family == 0 ? 0 : 1, key_bytes, pay, mode, layout)
                                  : rss_pick(int(n), sp.family == 0 ? 0 : 1, key_bytes, pay, mode, layout);

@@ -557,7 +557,13 @@ int launch_segments(const nsg_spec& sp, const uint32_t* offsets, int64_t nseg, c
   e = cudaLaunchKernel(k.fn, dim3(unsigned(grid)), dim3(kThreads), args, size_t(k.smem), st);
   if (e != cudaSuccess) return fail(NSG_ERR_CUDA, "seg_kernel launch: %s", cudaGetErrorString(e));
   // long segments (17..1024 items): warp RSS over the device-side list
-  return launch_rss_segment_list(sp, offsets, w + 4, w, w + 1, int64_t(cap), keys_in, keys_out, pay_in, pay_out, st);
+  if (int rc = launch_rss_segment_list(sp, offsets, w + 4, w, w + 1, int64_t(cap), keys_in, keys_out, pay_in, pay_out,
+                                       st))
+    return rc;
+  // longer ones (keys-only / UNIQUE): one CTA each over the same list
+  if (sp.payload_dtype != NSG_PAY_NONE && sp.tie_mode != NSG_TIE_UNIQUE) return 0;
+  return launch_bigsort_segment_list(offsets, w + 4, w, w + 1, int64_t(cap), 1024, keys_in, keys_out, pay_in, pay_out,
+                                     kb, sp.payload_dtype, xf, st);
 }
 
 }  // namespace nsg

@@ -167,17 +167,32 @@ def test_segments_unaligned_offsets(shift, torch):
     assert np.array_equal(gp.cpu().numpy().view(np.uint32), ep)
 
 
-def test_segments_longer_than_1024_fail_loudly(torch):
-    """Segments > 1024 items are beyond the device sorters: the call raises
-    (nsg_segments_check) instead of returning unsorted data silently."""
-    from paper_2002_05599_b200 import batch
+def test_segments_longer_than_1024(torch):
+    """Keys-only / UNIQUE segments above 1024 items go to the CTA sorter
+    (csrc/bigsort.cu) up to its shared-memory capacity; REF mode with a
+    payload stops at 1024 and beyond-capacity segments fail loudly
+    (nsg_segments_check) instead of returning unsorted data."""
     from paper_2002_05599_b200.errors import ConfigurationError
-    off = _csr(np.array([5, 1025, 3], dtype=np.uint32))
-    keys = np.arange(int(off[-1]), dtype=np.uint32)[::-1].copy()
-    with pytest.raises(ConfigurationError, match="longer than 1024"):
-        _run(torch, off, keys, None)
-    off = _csr(np.array([5, 1024, 3], dtype=np.uint32))
-    keys = np.arange(int(off[-1]), dtype=np.uint32)[::-1].copy()
+    rng = np.random.default_rng(1025)
+    lengths = np.array([5, 1025, 3, 0, 20000, 1, 4096, 17, 1024], dtype=np.uint32)
+    off = _csr(lengths)
+    keys = rng.integers(0, 2**32, size=int(off[-1]), dtype=np.uint64).astype(np.uint32)
+    keys[::3] %= 11
     gk, _ = _run(torch, off, keys, None)
     ek, _ = oracle.typed_sort_segments(off, keys, None)
     assert np.array_equal(gk, ek)
+    off = _csr(np.array([5, 1025, 3, 0, 9000, 1, 4096, 17, 1024], dtype=np.uint32))  # <= 16384 8-byte items
+    keys = keys[: int(off[-1])].copy()
+    pay = rng.integers(0, 2**32, size=int(off[-1]), dtype=np.uint64).astype(np.uint32)
+    for desc in (False, True):
+        gk, gp = _run(torch, off, keys, pay, tie="unique", descending=desc)
+        ek, ep = oracle.typed_sort_segments(off, keys, pay, unique=True, descending=desc)
+        assert np.array_equal(gk, ek) and np.array_equal(gp, ep), desc
+    # REF mode with a payload: the reference's tie order is replayed up to 1024
+    with pytest.raises(ConfigurationError, match="device limit"):
+        _run(torch, _csr(np.array([5, 1025, 3], dtype=np.uint32)),
+             np.arange(1033, dtype=np.uint32)[::-1].copy(), np.arange(1033, dtype=np.uint32), tie="ref")
+    # above the CTA sorter's shared-memory capacity (32768 4-byte keys)
+    off = _csr(np.array([5, 40000, 3], dtype=np.uint32))
+    with pytest.raises(ConfigurationError, match="device limit"):
+        _run(torch, off, np.arange(int(off[-1]), dtype=np.uint32)[::-1].copy(), None)

@@ -92,6 +92,7 @@ __device__ void smem_sort(const U* ksrc, const P* psrc, U* kdst, P* pdst, int le
   P* sp = reinterpret_cast<P*>(smem + C::CAP * sizeof(U));
   int np = 2;
   while (np < len) np <<= 1;
+  NSG_DCHECK(np <= C::CAP);
   for (int i = threadIdx.x; i < np; i += kBigThreads) {
     if (i < len) {
       sk[i] = ord_in ? ksrc[i] : ord_k<U, P>(ksrc[i], xf);
@@ -177,6 +178,7 @@ __device__ void merge_pass(const U* sk, const P* sp, U* dk, P* dp, int64_t len, 
       const int64_t d = o - r0;
       int64_t ai = merge_split<U, P>(ak, ap, na, bk, bp, nb, d);
       int64_t bi = d - ai;
+      NSG_DCHECK(ai >= 0 && ai <= na && bi >= 0 && bi <= nb);
       for (int q = 0; q < kMergePer && o + q < r0 + na + nb; ++q) {
         bool take_a;
         if (ai >= na) {

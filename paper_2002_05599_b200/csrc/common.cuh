@@ -9,11 +9,33 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <type_traits>
 
 #include <cuda_runtime.h>
 
 namespace nsg {
+
+// Bounds / invariant checks of a CHECKED build (-DNSG_CHECKED=1: the
+// compute-sanitizer substitute, see tools/sanitize_probe.py); compiled out of
+// the product build.
+#ifndef NSG_CHECKED
+#define NSG_CHECKED 0
+#endif
+#if NSG_CHECKED
+#define NSG_DCHECK(cond)                                                                          \
+  do {                                                                                            \
+    if (!(cond)) {                                                                                \
+      printf("NSG_DCHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__, __LINE__, \
+             int(blockIdx.x), int(threadIdx.x));                                                 \
+      __trap();                                                                                   \
+    }                                                                                             \
+  } while (0)
+#else
+#define NSG_DCHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
 
 struct NoPay {};
 

@@ -346,6 +346,7 @@ struct PhaseRss {
     cnt[lane] = 0u;
     __syncwarp();
     // ---- sample + splitters ------------------------------------------------
+    NSG_DCHECK(c.spos < uint32_t(c.n));
     uint32_t s = c.rowv ? prow[c.spos] : 0xffffffffu;
 #pragma unroll
     for (int k2 = 2; k2 <= L; k2 <<= 1) {
@@ -385,7 +386,11 @@ struct PhaseRss {
     __syncwarp();
 #pragma unroll
     for (int r = 0; r < E; ++r) {
-      if (r < c.rl) pb[atomicAdd(&cnt[q[r]], 1u)] = pk[r];
+      if (r < c.rl) {
+        const uint32_t dst = atomicAdd(&cnt[q[r]], 1u);
+        NSG_DCHECK(dst >= uint32_t(g * NR) && dst < uint32_t(g * NR + c.n));
+        pb[dst] = pk[r];
+      }
     }
     __syncwarp();
     // ---- base case: 8-word blocks, network, merge-split rounds ---------------
@@ -596,6 +601,7 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
       if (FULL || r < rl) {
         const int q = ll + L * r;  // q / E folds to (L*r)/E when L <= E
         const uint32_t idx = pr[L <= E ? q + (L * r) / E : q + q / E] & uint32_t(NR - 1);
+        NSG_DCHECK(!rowv || int(idx) < n);
         ok[r] = rk[idx];
         if constexpr (HAS_P) op[r] = rp[idx];
       }

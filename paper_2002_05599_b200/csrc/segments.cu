@@ -416,6 +416,7 @@ __global__ void __launch_bounds__(kThreads, NSG_SEG_MINB) seg_kernel(const SegPa
         if (j < nshort) {
           const int s = a + perm[j];
           const int st = int(offs[s] - e0);
+          NSG_DCHECK(st >= 0 && int(offs[s + 1] - e0) <= G::CAP);
           sort_segment_smem<U, P, DAG, CX, XK>(reinterpret_cast<U*>(kb) + st, reinterpret_cast<P*>(pb) + st,
                                                int(offs[s + 1] - offs[s]), xf);
         }

@@ -419,6 +419,9 @@ def main():
     from paper_2002_05599_b200 import _lib, batch, registry
     grp = Group()
     world, rank, local = grp.world, grp.rank, grp.local
+    # one GPU per rank; more ranks than GPUs (the 2-rank GPU test on a 1-GPU
+    # box) share devices -- safe here: no kernel waits on another rank
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     lib = _lib.lib()

@@ -52,6 +52,11 @@ int launch_bigsort_segment_list(const uint32_t* offsets, const uint32_t* ids, co
                                 const void* p_in, void* p_out, int key_bytes, int pay, const Xform& xf,
                                 cudaStream_t st);
 
+// netbulk.cu (odd-width u64 rows, TMA bulk-staged network sort)
+bool netbulk_covers(int n, int dag, int key_bytes, int pay);
+int launch_netbulk(int n, int dag, int pay, int mode, const void* k_in, void* k_out, const void* p_in, void* p_out,
+                   int64_t rows, const Xform& xf, cudaStream_t st);
+
 // wmerge.cu
 int launch_wmerge(const nsg_spec& sp, const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows,
                   int64_t n, cudaStream_t st);

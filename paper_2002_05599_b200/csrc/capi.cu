@@ -216,9 +216,16 @@ int nsg_sort_rows(const nsg_spec* sp, const void* keys_in, void* keys_out, const
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (sp->kind == NSG_KIND_NETWORK) {
     if (n > 16) return fail(NSG_ERR_SPEC, "network sorters cover 2..16 items, got %lld", (long long)n);
-    if (netbulk_covers(int(n), dag_of(*sp), kb, sp->payload_dtype) && !env_flag("NSG_NET_TILE_ONLY"))
-      return launch_netbulk(int(n), dag_of(*sp), sp->payload_dtype, sp->tie_mode, keys_in, keys_out, pay_in, pay_out,
-                            rows, make_xform(*sp), st);
+    if (nettma_covers(int(n), kb, sp->payload_dtype) && !env_flag("NSG_NET_TILE_ONLY")) {
+      const int rc = launch_nettma(dag_of(*sp), sp->payload_dtype, sp->tie_mode, keys_in, keys_out, pay_in, pay_out,
+                                   rows, make_xform(*sp), st);
+      if (rc != -4) return rc;
+    }
+    if (netbulk_covers(int(n), dag_of(*sp), kb, sp->payload_dtype) && !env_flag("NSG_NET_TILE_ONLY")) {
+      const int rc = launch_netbulk(int(n), dag_of(*sp), sp->payload_dtype, sp->tie_mode, keys_in, keys_out, pay_in,
+                                    pay_out, rows, make_xform(*sp), st);
+      if (rc != -4) return rc;
+    }
     NetParams prm{keys_in, keys_out, pay_in, pay_out, rows, make_xform(*sp)};
     const KernelInfo k = net_lookup(int(n), dag_of(*sp), kb, sp->payload_dtype, sp->tie_mode, LAYOUT_SOA);
     return launch_net(k, prm, st);

@@ -57,6 +57,11 @@ bool netbulk_covers(int n, int dag, int key_bytes, int pay);
 int launch_netbulk(int n, int dag, int pay, int mode, const void* k_in, void* k_out, const void* p_in, void* p_out,
                    int64_t rows, const Xform& xf, cudaStream_t st);
 
+// nettma.cu (16-item u64 rows, TMA tensor copies with hardware swizzle); -4 = not served
+bool nettma_covers(int n, int key_bytes, int pay);
+int launch_nettma(int dag, int pay, int mode, const void* k_in, void* k_out, const void* p_in, void* p_out,
+                  int64_t rows, const Xform& xf, cudaStream_t st);
+
 // wmerge.cu
 int launch_wmerge(const nsg_spec& sp, const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows,
                   int64_t n, cudaStream_t st);

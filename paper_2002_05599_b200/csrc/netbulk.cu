@@ -11,6 +11,8 @@
 // conflict-free without a swizzle -- runs the network (same DAG and
 // compare-exchange as net_sort.cuh), writes the row back, and one bulk store
 // per region returns the group.
+#include <cstdlib>
+
 #include "bulk.cuh"
 #include "common.cuh"
 #include "gen/nets.cuh"
@@ -32,6 +34,7 @@ struct NbKnobs {
 };
 using NbA = NbKnobs<2, 49152, 4>;
 using NbB = NbKnobs<1, 16384, 8>;
+using NbC = NbKnobs<4, 57344, 4>;  // short rows: bigger groups, deeper ring (tuning: NSG_NB_FORCE=3)
 
 template <int N, class U, class P, class K>
 struct NbCfg {
@@ -175,6 +178,9 @@ template <int N, int DAG, class U, class P, class K>
 NbLaunch nb_mode(int mode) {
   using C = NbCfg<N, U, P, K>;
   NbLaunch l;
+  if constexpr (C::CTA_SMEM > 227 * 1024) {
+    return l;  // this configuration does not fit the shape: the tile kernel serves it
+  }
   l.smem = C::CTA_SMEM;
   l.warps = C::WARPS;
   l.rows_per_warp = C::ROWS;
@@ -196,12 +202,27 @@ constexpr int nb_choice(int n, int dag, int pay) {
   return 0;
 }
 
+// tuning override: NSG_NB_FORCE=1|2|3 runs every odd n in 5..15 on A / B / C
+int nb_force() {
+  static const int f = [] {
+    const char* e = getenv("NSG_NB_FORCE");
+    return e ? atoi(e) : 0;
+  }();
+  return f;
+}
+
+template <int N, int DAG, class P>
+NbLaunch nb_cfg(int c, int mode) {
+  if (c == 1) return nb_mode<N, DAG, uint64_t, P, NbA>(mode);
+  if (c == 2) return nb_mode<N, DAG, uint64_t, P, NbB>(mode);
+  if (c == 3) return nb_mode<N, DAG, uint64_t, P, NbC>(mode);
+  return NbLaunch{};
+}
+
 template <int N, int DAG>
 NbLaunch nb_pick(int pay, int mode) {
-  const int c = nb_choice(N, DAG, pay);
-  if (c == 0) return NbLaunch{};
-  if (pay == 0) return c == 1 ? nb_mode<N, DAG, uint64_t, NoPay, NbA>(mode) : nb_mode<N, DAG, uint64_t, NoPay, NbB>(mode);
-  return c == 1 ? nb_mode<N, DAG, uint64_t, uint32_t, NbA>(mode) : nb_mode<N, DAG, uint64_t, uint32_t, NbB>(mode);
+  const int c = nb_force() ? nb_force() : nb_choice(N, DAG, pay);
+  return pay == 0 ? nb_cfg<N, DAG, NoPay>(c, mode) : nb_cfg<N, DAG, uint32_t>(c, mode);
 }
 
 template <int N>
@@ -211,6 +232,8 @@ NbLaunch nb_dag(int dag, int pay, int mode) {
 
 NbLaunch nb_lookup(int n, int dag, int pay, int mode) {
   switch (n) {
+    case 5: return nb_dag<5>(dag, pay, mode);
+    case 7: return nb_dag<7>(dag, pay, mode);
     case 9: return nb_dag<9>(dag, pay, mode);
     case 11: return nb_dag<11>(dag, pay, mode);
     case 13: return nb_dag<13>(dag, pay, mode);
@@ -224,14 +247,14 @@ NbLaunch nb_lookup(int n, int dag, int pay, int mode) {
 // u64 keys (+ u32 payload), SoA, the odd widths where the bulk-staged kernel
 // measured faster than the cp.async tile pipeline
 bool netbulk_covers(int n, int dag, int key_bytes, int pay) {
-  return key_bytes == 8 && (pay == 0 || pay == 1) && (n & 1) && n >= 9 && n <= 15 &&
-         nb_choice(n, dag ? 1 : 0, pay) != 0;
+  return key_bytes == 8 && (pay == 0 || pay == 1) && (n & 1) && n >= 5 && n <= 15 &&
+         (nb_force() != 0 || nb_choice(n, dag ? 1 : 0, pay) != 0);
 }
 
 int launch_netbulk(int n, int dag, int pay, int mode, const void* k_in, void* k_out, const void* p_in, void* p_out,
                    int64_t rows, const Xform& xf, cudaStream_t st) {
   const NbLaunch l = nb_lookup(n, dag ? 1 : 0, pay, mode);
-  if (!l.fn) return fail(NSG_ERR_SPEC, "no bulk-staged network kernel for n=%d", n);
+  if (!l.fn) return -4;  // not served here (caller falls back to the tile kernel)
   if (rows <= 0) return 0;
   int sms = 0, occ = 0;
   const int threads = l.warps * 32;

@@ -112,6 +112,16 @@ class Cell:
     def kernel_key(self) -> str:  # name used by tools/profile_summary.py / profiles/traffic.json
         fam = "best" if self.family == "best" else "bn"
         pay = {0: "keys", 4: "p32", 8: "p64"}[self.pb]
+        kt = "u64" if self.kb == 8 else "u32"
+        # staged by TMA (mirrors csrc/capi.cu dispatch: nettma_covers, netbulk.cu nb_choice)
+        if self.kb == 8 and self.n == 16 and self.pb == 4:
+            return f"nettma n=16 {fam} {kt} {pay} SoA UNIQUE"
+        if self.kb == 8 and self.pb in (0, 4) and self.n % 2 and 9 <= self.n <= 15:
+            d = 0 if self.family == "best" else 1
+            bulk = (self.n in (11, 13) or (self.n == 15 and d == 0)) if self.pb == 0 else \
+                (self.n in (9, 11) or (self.n == 13 and d == 0) or self.n == 15)
+            if bulk:
+                return f"netbulk n={self.n} {fam} {kt} {pay} SoA UNIQUE"
         # rows of <= 64 bytes per region run the register-direct kernel
         # (net_direct_kernel, csrc/net_sort.cuh direct_row_ok)
         ok = lambda r: r <= 16 or r == 24 or (r % 16 == 0 and r <= 64)  # noqa: E731

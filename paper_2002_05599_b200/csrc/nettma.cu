@@ -83,6 +83,71 @@ __device__ __forceinline__ int swz_off(int r, int c) {
   }
 }
 
+template <class P>
+__device__ __forceinline__ void nt_load_row(const unsigned char* ks, const unsigned char* ps, int r,
+                                            Elem<uint64_t, P> (&v)[16]) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const uint4 x = *reinterpret_cast<const uint4*>(ks + swz_off<128>(r, c));
+    v[2 * c].k = uint64_t(x.x) | (uint64_t(x.y) << 32);
+    v[2 * c + 1].k = uint64_t(x.z) | (uint64_t(x.w) << 32);
+  }
+  if constexpr (!IsNoPay<P>::value) {
+    if constexpr (sizeof(P) == 4) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint4 x = *reinterpret_cast<const uint4*>(ps + swz_off<64>(r, c));
+        v[4 * c].p = x.x;
+        v[4 * c + 1].p = x.y;
+        v[4 * c + 2].p = x.z;
+        v[4 * c + 3].p = x.w;
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const uint4 x = *reinterpret_cast<const uint4*>(ps + swz_off<128>(r, c));
+        v[2 * c].p = uint64_t(x.x) | (uint64_t(x.y) << 32);
+        v[2 * c + 1].p = uint64_t(x.z) | (uint64_t(x.w) << 32);
+      }
+    }
+  }
+}
+
+template <class P>
+__device__ __forceinline__ void nt_store_row(unsigned char* ks, unsigned char* ps, int r,
+                                             const Elem<uint64_t, P> (&v)[16]) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    *reinterpret_cast<uint4*>(ks + swz_off<128>(r, c)) = make_uint4(
+        uint32_t(v[2 * c].k), uint32_t(v[2 * c].k >> 32), uint32_t(v[2 * c + 1].k), uint32_t(v[2 * c + 1].k >> 32));
+  }
+  if constexpr (!IsNoPay<P>::value) {
+    if constexpr (sizeof(P) == 4) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        *reinterpret_cast<uint4*>(ps + swz_off<64>(r, c)) =
+            make_uint4(v[4 * c].p, v[4 * c + 1].p, v[4 * c + 2].p, v[4 * c + 3].p);
+    } else {
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        *reinterpret_cast<uint4*>(ps + swz_off<128>(r, c)) =
+            make_uint4(uint32_t(v[2 * c].p), uint32_t(v[2 * c].p >> 32), uint32_t(v[2 * c + 1].p),
+                       uint32_t(v[2 * c + 1].p >> 32));
+    }
+  }
+}
+
+// to / from the order-preserving space (keys; payloads in UNIQUE mode)
+template <class P, int MODE>
+__device__ __forceinline__ void nt_xform(Elem<uint64_t, P> (&v)[16], const Xform& xf, bool to) {
+  if (!xf.active) return;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    v[j].k = to ? to_ord<uint64_t>(v[j].k, xf) : from_ord<uint64_t>(v[j].k, xf);
+    if constexpr (!IsNoPay<P>::value && MODE == MODE_UNIQUE) v[j].p ^= P(xf.pdesc);
+  }
+}
+
 template <int DAG, class P, int MODE>
 __global__ void __launch_bounds__(NSG_NT_WARPS * 32) nettma_kernel(const __grid_constant__ CUtensorMap tk,
                                                                    const __grid_constant__ CUtensorMap tp,
@@ -139,70 +204,35 @@ __global__ void __launch_bounds__(NSG_NT_WARPS * 32) nettma_kernel(const __grid_
     unsigned char* ps = ks + C::KB;
     mbar_wait_parity(&bar[b], (phases >> b) & 1u);
     phases ^= 1u << b;
+    if constexpr (NSG_NT_APL == 2) {  // two rows per lane, networks interleaved (ILP for one warp per scheduler)
+      Elem<U, P> v0[N], v1[N];
+      nt_load_row<P>(ks, ps, lane, v0);
+      nt_load_row<P>(ks, ps, lane + 32, v1);
+      nt_xform<P, MODE>(v0, xf, true);
+      nt_xform<P, MODE>(v1, xf, true);
+      RowPair<Elem<U, P>> w[N];
 #pragma unroll
-    for (int rr = 0; rr < NSG_NT_APL; ++rr) {
-      const int r = rr * 32 + lane;
+      for (int j = 0; j < N; ++j) {
+        w[j].a = v0[j];
+        w[j].b = v1[j];
+      }
+      Net<DAG, N>::template run<CxPair<CX>>(w);
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        v0[j] = w[j].a;
+        v1[j] = w[j].b;
+      }
+      nt_xform<P, MODE>(v0, xf, false);
+      nt_xform<P, MODE>(v1, xf, false);
+      nt_store_row<P>(ks, ps, lane, v0);
+      nt_store_row<P>(ks, ps, lane + 32, v1);
+    } else {
       Elem<U, P> v[N];
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const uint4 x = *reinterpret_cast<const uint4*>(ks + swz_off<128>(r, c));
-        v[2 * c].k = uint64_t(x.x) | (uint64_t(x.y) << 32);
-        v[2 * c + 1].k = uint64_t(x.z) | (uint64_t(x.w) << 32);
-      }
-      if constexpr (HAS_P) {
-        if constexpr (sizeof(P) == 4) {
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const uint4 x = *reinterpret_cast<const uint4*>(ps + swz_off<64>(r, c));
-            v[4 * c].p = x.x;
-            v[4 * c + 1].p = x.y;
-            v[4 * c + 2].p = x.z;
-            v[4 * c + 3].p = x.w;
-          }
-        } else {
-#pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const uint4 x = *reinterpret_cast<const uint4*>(ps + swz_off<128>(r, c));
-            v[2 * c].p = uint64_t(x.x) | (uint64_t(x.y) << 32);
-            v[2 * c + 1].p = uint64_t(x.z) | (uint64_t(x.w) << 32);
-          }
-        }
-      }
-      if (xf.active) {
-#pragma unroll
-        for (int j = 0; j < N; ++j) {
-          v[j].k = to_ord<U>(v[j].k, xf);
-          if constexpr (HAS_P && MODE == MODE_UNIQUE) v[j].p ^= P(xf.pdesc);
-        }
-      }
+      nt_load_row<P>(ks, ps, lane, v);
+      nt_xform<P, MODE>(v, xf, true);
       Net<DAG, N>::template run<CX>(v);
-      if (xf.active) {
-#pragma unroll
-        for (int j = 0; j < N; ++j) {
-          v[j].k = from_ord<U>(v[j].k, xf);
-          if constexpr (HAS_P && MODE == MODE_UNIQUE) v[j].p ^= P(xf.pdesc);
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        *reinterpret_cast<uint4*>(ks + swz_off<128>(r, c)) =
-            make_uint4(uint32_t(v[2 * c].k), uint32_t(v[2 * c].k >> 32), uint32_t(v[2 * c + 1].k),
-                       uint32_t(v[2 * c + 1].k >> 32));
-      }
-      if constexpr (HAS_P) {
-        if constexpr (sizeof(P) == 4) {
-#pragma unroll
-          for (int c = 0; c < 4; ++c)
-            *reinterpret_cast<uint4*>(ps + swz_off<64>(r, c)) =
-                make_uint4(v[4 * c].p, v[4 * c + 1].p, v[4 * c + 2].p, v[4 * c + 3].p);
-        } else {
-#pragma unroll
-          for (int c = 0; c < 8; ++c)
-            *reinterpret_cast<uint4*>(ps + swz_off<128>(r, c)) =
-                make_uint4(uint32_t(v[2 * c].p), uint32_t(v[2 * c].p >> 32), uint32_t(v[2 * c + 1].p),
-                           uint32_t(v[2 * c + 1].p >> 32));
-        }
-      }
+      nt_xform<P, MODE>(v, xf, false);
+      nt_store_row<P>(ks, ps, lane, v);
     }
     fence_proxy_async_smem();
     __syncwarp();

@@ -54,6 +54,21 @@ def short_name(name: str) -> str:
         pt = {"NoPay": "keys", "unsigned int": "p32", "unsigned long": "p64"}.get(p.strip(), p)
         kind = "net_direct" if "net_direct_kernel" in name else "net_sort"
         return f"{kind} n={n} {fam} {kt} {pt} {'AoS' if lay == '1' else 'SoA'} {'UNIQUE' if mode == '1' else 'REF'}"
+    pay_name = lambda p: {"NoPay": "keys", "unsigned int": "p32", "unsigned long": "p64"}.get(  # noqa: E731
+        re.sub(r"^(?:nsg::)?", "", p.strip()), p.strip())
+    m = re.search(rf"netbulk_kernel<{I}(\d+), {I}(\d), unsigned long, ((?:nsg::)?[A-Za-z ]+?), {I}(\d)", name)
+    if m:
+        n, dag, p, mode = m.groups()
+        return f"netbulk n={n} {'best' if dag == '0' else 'bn'} u64 {pay_name(p)} SoA {'UNIQUE' if mode == '1' else 'REF'}"
+    m = re.search(rf"nettma_kernel<{I}(\d), ((?:nsg::)?[A-Za-z ]+?), {I}(\d)>", name)
+    if m:
+        dag, p, mode = m.groups()
+        return f"nettma n=16 {'best' if dag == '0' else 'bn'} u64 {pay_name(p)} SoA {'UNIQUE' if mode == '1' else 'REF'}"
+    m = re.search(r"pksort_kernel<unsigned (long|int), ((?:nsg::)?[A-Za-z ]+?), (?:\(int\))?(\d), (?:\(int\))?(\d+), "
+                  r"(?:\(bool\))?(\d|true|false), (?:nsg::)?(?:<unnamed>::)?(?:unnamed>::)?Phase(Bitonic|Rss)", name)
+    if m:
+        u, p, lg, e, full, ph = m.groups()
+        return f"pksort {'merge' if ph == 'Bitonic' else 'rss'} NR={1 << int(lg)} {'u64' if u == 'long' else 'u32'} {pay_name(p)}"
     return name[:90]
 
 

@@ -24,6 +24,7 @@
 //     (RSS 332 with the spec's network family as base case; <= 1024 items).
 //     Tiles whose element range exceeds the staging buffer are processed in
 //     synchronous sub-tiles.
+#include "bulk.cuh"
 #include "common.cuh"
 #include "gen/nets.cuh"
 #include "kernels.cuh"
@@ -84,7 +85,8 @@ struct SegGeom {
   static constexpr int OFF_OFFS = 0;                                   // 3 slots
   static constexpr int OFF_PERM = OFF_OFFS + 3 * OFFS_STRIDE * 4;      // TS_ u16
   static constexpr int OFF_HIST = OFF_PERM + TS_ * 2;            // 32 int
-  static constexpr int OFF_DATA = (OFF_HIST + 32 * 4 + 15) / 16 * 16;  // 2 buffers
+  static constexpr int OFF_BAR = (OFF_HIST + 32 * 4 + 7) / 8 * 8;        // 2 mbarriers (bulk tile loads)
+  static constexpr int OFF_DATA = (OFF_BAR + 2 * 8 + 15) / 16 * 16;       // 2 buffers
   static constexpr int SMEM = OFF_DATA + 2 * BUF;
 };
 
@@ -115,6 +117,22 @@ __device__ __forceinline__ void issue_range(unsigned char* dst, const unsigned c
     cp_async16(dst + off, nb ? gbase + off : gbase, nb);
   }
 }
+// The same range as ONE TMA bulk copy (issued by the calling thread),
+// completing on `bar`, when every 16-byte chunk of it is readable; returns
+// the bytes it will deliver (0: not possible, use issue_range).
+template <int EB>
+__device__ __forceinline__ unsigned range_chunks_bytes(uint32_t e0, uint32_t e1, uint64_t limit_bytes) {
+  const uint64_t c0 = (uint64_t(e0) * EB) >> 4;
+  const uint64_t nch = ((uint64_t(e1) * EB + 15) >> 4) - c0;
+  return int64_t(limit_bytes) - int64_t(c0 << 4) >= int64_t(nch) * 16 ? unsigned(nch * 16) : 0u;
+}
+template <int EB>
+__device__ __forceinline__ void bulk_range(unsigned char* dst, const unsigned char* src, uint32_t e0, unsigned bytes,
+                                           uint64_t* bar) {
+  const uint64_t c0 = (uint64_t(e0) * EB) >> 4;
+  bulk_g2s(dst, src + (c0 << 4), bytes, bar);
+}
+
 template <int EB>
 __device__ __forceinline__ int range_shift(uint32_t e0) {
   return int((uint64_t(e0) * EB) & 15);
@@ -155,6 +173,32 @@ __device__ __forceinline__ void store_range(const unsigned char* sm, T* dst, uin
     for (int i = 0; i < 16 / EB; ++i) u.e[i] = f(u.e[i]);
     stg128_cs(g16 + (c << 4), u.v);
   }
+}
+
+// store_range with the 16-byte aligned interior as ONE TMA bulk store issued
+// by thread 0 (the caller fences the generic writes and synchronises first);
+// the partial edge chunks shared with the neighbouring tiles stay element
+// stores.  The staging buffer may be refilled only after
+// cp.async.bulk.wait_group.read.
+template <class T>
+__device__ __forceinline__ void store_range_bulk(const unsigned char* sm, T* dst, uint32_t e0, uint32_t e1, int tid) {
+  constexpr int EB = int(sizeof(T));
+  const uint64_t b0 = uint64_t(e0) * EB, b1 = uint64_t(e1) * EB;
+  const uint64_t base = b0 & ~uint64_t(15);
+  uint64_t h_end = (b0 + 15) & ~uint64_t(15);
+  if (h_end > b1) h_end = b1;
+  uint64_t t_beg = b1 & ~uint64_t(15);
+  if (t_beg < h_end) t_beg = h_end;
+  unsigned char* g = reinterpret_cast<unsigned char*>(dst);
+  const int nhead = int(h_end - b0) / EB, ntail = int(b1 - t_beg) / EB;
+  if (tid >= 64 && tid < 64 + nhead) {
+    const uint64_t b = b0 + uint64_t(tid - 64) * EB;
+    *reinterpret_cast<T*>(g + b) = *reinterpret_cast<const T*>(sm + (b - base));
+  } else if (tid >= 96 && tid < 96 + ntail) {
+    const uint64_t b = t_beg + uint64_t(tid - 96) * EB;
+    *reinterpret_cast<T*>(g + b) = *reinterpret_cast<const T*>(sm + (b - base));
+  }
+  if (tid == 0 && t_beg > h_end) bulk_s2g(g + h_end, sm + (h_end - base), unsigned(t_beg - h_end));
 }
 
 // Order transform kinds (template XK): none, generic, float descending.  The
@@ -352,6 +396,26 @@ __global__ void __launch_bounds__(kThreads, NSG_SEG_MINB) seg_kernel(const SegPa
     issue_range<int(sizeof(U))>(buf, kin, e0, e1, klimit, tid);
     if constexpr (HAS_P) issue_range<G::PB>(buf + G::K_REG, pin, e0, e1, plimit, tid);
   };
+  // prefetched tiles: one TMA bulk copy per region when the 16-byte chunk
+  // cover of the range is readable (every tile but possibly the array's
+  // last), issued by thread 0 and completed on the slot's mbarrier --
+  // returns whether it did (uniform: every thread computes the same)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + G::OFF_BAR);
+  auto issue_data_bulk = [&](int slot, uint32_t e0, uint32_t e1) -> bool {
+    const unsigned kbytes = range_chunks_bytes<int(sizeof(U))>(e0, e1, klimit);
+    const unsigned pbytes = HAS_P ? range_chunks_bytes<G::PB>(e0, e1, plimit) : 0u;
+    if (!kbytes || (HAS_P && !pbytes)) {
+      issue_data(data_slot(slot), e0, e1);
+      return false;
+    }
+    if (tid == 0) {
+      unsigned char* buf = data_slot(slot);
+      mbar_expect_tx(&bars[slot & 1], kbytes + pbytes);
+      bulk_range<int(sizeof(U))>(buf, kin, e0, kbytes, &bars[slot & 1]);
+      if constexpr (HAS_P) bulk_range<G::PB>(buf + G::K_REG, pin, e0, pbytes, &bars[slot & 1]);
+    }
+    return true;
+  };
 
   // Bin + sort + store the segments [a, b) of a tile whose elements
   // [offs[a], offs[b]) are staged in `buf` (or, if !staged, only collect longs).
@@ -422,11 +486,14 @@ __global__ void __launch_bounds__(kThreads, NSG_SEG_MINB) seg_kernel(const SegPa
         }
       }
     }
+    // this thread's generic writes of `buf` before the copy engine reads it
+    fence_proxy_async_smem();
     __syncthreads();
     if (tid < 32) hist[tid] = 0;  // ready for the next call (after its leading sync)
     if (staged) {  // (elements are back in their own representation)
-      store_range<U>(buf, kout, e0, e1, tid, [](U k) { return k; });
-      if constexpr (HAS_P) store_range<P>(buf + G::K_REG, pout, e0, e1, tid, [](P q) { return q; });
+      store_range_bulk<U>(buf, kout, e0, e1, tid);
+      if constexpr (HAS_P) store_range_bulk<P>(buf + G::K_REG, pout, e0, e1, tid);
+      if (tid == 0) bulk_commit();
     }
     // no trailing barrier: the next tile starts with wait + __syncthreads
   };
@@ -434,6 +501,13 @@ __global__ void __launch_bounds__(kThreads, NSG_SEG_MINB) seg_kernel(const SegPa
   int t = int(blockIdx.x);
   if (t >= ntiles) return;
   if (tid < 32) hist[tid] = 0;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_init_fence();
+  }
+  uint32_t bulk_pending = 0, phases = 0;  // per slot: a bulk load is in flight / its parity
+  __syncthreads();
   // prologue: offsets of tile 0 (synchronously), data of tile 0 + offsets of tile 1 (async)
   issue_offs(t, offs_slot(0));
   cp_async_commit();
@@ -442,12 +516,17 @@ __global__ void __launch_bounds__(kThreads, NSG_SEG_MINB) seg_kernel(const SegPa
   {
     const uint32_t* o = offs_slot(0);
     const int nts = nsegs_of(t);
-    if (o[nts] - o[0] <= uint32_t(G::CAP)) issue_data(data_slot(0), o[0], o[nts]);
+    if (o[nts] - o[0] <= uint32_t(G::CAP) && issue_data_bulk(0, o[0], o[nts])) bulk_pending |= 1u;
     if (t + gstride < ntiles) issue_offs(t + gstride, offs_slot(1));
     cp_async_commit();
   }
   for (int k = 0; t < ntiles; ++k, t += gstride) {
     cp_async_wait<0>();
+    if (bulk_pending & (1u << (k & 1))) {
+      mbar_wait_parity(&bars[k & 1], (phases >> (k & 1)) & 1u);
+      phases ^= 1u << (k & 1);
+      bulk_pending &= ~(1u << (k & 1));
+    }
     __syncthreads();
     const uint32_t* offs = offs_slot(k);
     const int nts = nsegs_of(t);
@@ -455,8 +534,10 @@ __global__ void __launch_bounds__(kThreads, NSG_SEG_MINB) seg_kernel(const SegPa
     const int tn = t + gstride;
     if (tn < ntiles) {  // prefetch: data of the next tile, offsets of the one after
       const uint32_t* on = offs_slot(k + 1);
+      if (tid == 0) bulk_wait_read<0>();  // the previous tile's bulk stores have read that slot
       const int ntn = nsegs_of(tn);
-      if (on[ntn] - on[0] <= uint32_t(G::CAP)) issue_data(data_slot(k + 1), on[0], on[ntn]);
+      if (on[ntn] - on[0] <= uint32_t(G::CAP) && issue_data_bulk(k + 1, on[0], on[ntn]))
+        bulk_pending |= 1u << ((k + 1) & 1);
       if (tn + gstride < ntiles) issue_offs(tn + gstride, offs_slot(k + 2));
     }
     cp_async_commit();
@@ -480,6 +561,7 @@ __global__ void __launch_bounds__(kThreads, NSG_SEG_MINB) seg_kernel(const SegPa
           b = lo;
         }
         staged = offs[b] - offs[a] <= uint32_t(G::CAP);
+        if (tid == 0) bulk_wait_read<0>();
         __syncthreads();  // previous sub-tile's stores have read `buf`
         if (staged) {
           issue_data(buf, offs[a], offs[b]);
@@ -493,6 +575,7 @@ __global__ void __launch_bounds__(kThreads, NSG_SEG_MINB) seg_kernel(const SegPa
     }
   }
   cp_async_wait<0>();
+  if (tid == 0) bulk_wait<0>();
 }
 
 struct SegKernel {

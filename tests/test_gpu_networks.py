@@ -399,3 +399,58 @@ def test_randomised_typed_networks_vs_oracle(seed, torch):
     assert np.array_equal(gk.cpu().numpy().view(np.uint8), ek.view(np.uint8)), cfg
     if pay is not None:
         assert np.array_equal(gp.cpu().numpy().view(pay.dtype), ep), cfg
+
+
+_TMA_SHAPES = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+from paper_2002_05599_b200 import batch
+import torch
+out = {{}}
+rng = np.random.default_rng(78)
+for n in (5, 7, 9, 11, 13, 15, 16):
+    for kdt, pdt in (("uint64", None), ("uint64", "uint32"), ("int64", "uint32"), ("float64", "uint64")):
+        for rows in (64 * 37 + 5, 100003):
+            keys = rng.integers(0, 5, size=(rows, n)).astype(kdt)
+            keys[::2] = rng.integers(-2**40, 2**40, size=keys[::2].shape).astype(kdt)
+            pay = None if pdt is None else rng.integers(0, 2**31, size=(rows, n)).astype(pdt)
+            tk = torch.from_numpy(keys).cuda() if kdt != "uint64" else \
+                torch.from_numpy(keys.view(np.int64)).cuda().view(torch.uint64)
+            tp = None
+            if pay is not None:
+                tp = torch.from_numpy(pay.view(np.int64 if pay.itemsize == 8 else np.int32)).cuda()
+                tp = tp.view(torch.uint64 if pay.itemsize == 8 else torch.uint32)
+            for tie in (("ref", "unique") if pay is not None else ("unique",)):
+                for fam in ("best", "bn-l"):
+                    k, p = batch.sort_rows(tk, tp, family=fam, tie=tie, descending=(rows % 2 == 1))
+                    key = f"{{n}}-{{kdt}}-{{pdt}}-{{rows}}-{{tie}}-{{fam}}"
+                    out[key] = (k.cpu().numpy().tobytes(), None if p is None else p.cpu().numpy().tobytes())
+import pickle
+sys.stdout.buffer.write(pickle.dumps(out))
+"""
+
+
+def test_tma_staged_and_tile_kernels_agree(torch):
+    """The TMA-staged kernels (netbulk.cu: odd n = 9..15 bulk copies;
+    nettma.cu: n = 16 u64 + u32 tensor copies with hardware swizzle) against
+    the cp.async tile kernel on the same rows (NSG_NET_TILE_ONLY=1): ragged
+    row counts (the bulk kernels' unaligned tails, the tensor copies' clipped
+    last box), REF and UNIQUE, signed / float / descending keys."""
+    import os
+    import pickle
+    import subprocess
+    import sys
+    root = str(Path(__file__).resolve().parent.parent)
+    code = _TMA_SHAPES.format(root=root)
+    runs = []
+    for tile_only in (False, True):
+        env = dict(os.environ)
+        env.pop("NSG_NET_TILE_ONLY", None)
+        if tile_only:
+            env["NSG_NET_TILE_ONLY"] = "1"
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, timeout=900)
+        assert r.returncode == 0, r.stderr.decode()[-2000:]
+        runs.append(pickle.loads(r.stdout))
+    assert runs[0].keys() == runs[1].keys() and len(runs[0]) > 50
+    for key in runs[0]:
+        assert runs[0][key] == runs[1][key], key

@@ -1,13 +1,13 @@
 """A/B of the bulk-staged odd-width network kernel (netbulk.cu) against the
 cp.async tile kernel (net_sort.cuh) on the cfg2 odd-n cells.
 
-    python tools/nb_variants.py [reps]     # on the GPU
+    python tools/nb_variants.py [reps] [force...]     # on the GPU
 
-Each round runs bench.py twice -- default dispatch, and NSG_NET_TILE_ONLY=1
-(every shape on the tile kernel) -- and prints GB/s per cell side by side.
-The per-shape choice in netbulk.cu (nb_choice) came from this sweep plus a
-knob sweep of rows per lane / ring bytes / warps per CTA (recorded in
-profiles/round2/netbulk.md).
+Each round runs bench.py with the default dispatch, with NSG_NET_TILE_ONLY=1
+(every shape on the tile kernel) and with NSG_NB_FORCE=<c> for each listed
+configuration c (1 = A, 2 = B, 3 = C in netbulk.cu: every odd n on that
+configuration), and prints GB/s per cell.  The per-shape choice in
+netbulk.cu (nb_choice) comes from these runs (profiles/round2/netbulk.md).
 """
 
 import json
@@ -31,6 +31,9 @@ def run(env_extra):
 
 if __name__ == "__main__":
     reps = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+    forces = sys.argv[2:]
     for i in range(reps):
-        a, b = run({}), run({"NSG_NET_TILE_ONLY": "1"})
-        print(json.dumps({"round": i, "default": a, "tile_only": b}), flush=True)
+        out = {"round": i, "default": run({}), "tile_only": run({"NSG_NET_TILE_ONLY": "1"})}
+        for f in forces:
+            out[f"force{f}"] = run({"NSG_NB_FORCE": f})
+        print(json.dumps(out), flush=True)

@@ -72,7 +72,8 @@ typedef struct {
  * (netsort_core.c:498-527).  `rows` is a DEVICE pointer to m*n packed
  * {uint64 key; uint64 ref} items (items.py:14), 16-byte aligned, sorted in
  * place row by row.  kind NETWORK: n in 2..16 (n < 2 is a no-op, else -2);
- * kind RSS: n <= 1024; kind INSERTION: stable by key, n <= 1024. */
+ * kind RSS: n <= 1024 (the reference's tie order, replayed draw for draw);
+ * kind INSERTION: stable by key, n <= 1024. */
 int nsg_run_sorter_many(const nsg_spec* sp, void* rows, int64_t m, int64_t n, void* stream);
 
 /* Same with HOST rows (pinned memory overlaps copies with sorting). */
@@ -80,7 +81,10 @@ int nsg_run_sorter_many_host(const nsg_spec* sp, void* rows, int64_t m, int64_t 
 
 /* Typed SoA batch: `rows` rows of n keys (key_dtype) and optional payloads
  * (payload_dtype), row-major, device pointers, 16-byte aligned.  Out-of-place
- * or in-place (out == in).  Network kinds: n 1..16.  RSS / INSERTION: n <= 1024. */
+ * or in-place (out == in).  Network kinds: n 1..16.  RSS and MERGE kinds,
+ * keys-only or UNIQUE: any n (n > 1024 through a CTA sorter; above its
+ * shared-memory capacity it allocates a stream-ordered scratch).  RSS with
+ * REF-mode payload order and INSERTION: n <= 1024. */
 int nsg_sort_rows(const nsg_spec* sp, const void* keys_in, void* keys_out, const void* pay_in, void* pay_out,
                   int64_t rows, int64_t n, void* stream);
 
@@ -90,11 +94,13 @@ int nsg_sort_rows_host(const nsg_spec* sp, const void* keys_in, void* keys_out, 
 
 /* Segmented (CSR) batch: segment s = [offsets[s], offsets[s+1]) of keys /
  * payloads; lengths 0..16 are sorted by the exact-length network of the spec's
- * family; lengths 17..1024 by the warp RSS sorter.  `ws` is a device workspace
- * of nsg_segments_ws_bytes(nseg, nelem) bytes.  Segments longer than 1024
- * items are NOT sorted: they are counted in the workspace, and
- * nsg_segments_check(ws) (which synchronises the stream) reports them as
- * NSG_ERR_SPEC -- call it unless every segment is known to be <= 1024. */
+ * family; lengths 17..1024 by the warp RSS sorter; longer ones (keys-only /
+ * UNIQUE) by a CTA sorter in shared memory up to its capacity (8192 16-byte,
+ * 16384 8-byte, 32768 4-byte items).  `ws` is a device workspace of
+ * nsg_segments_ws_bytes(nseg, nelem) bytes.  Segments beyond those limits
+ * (and REF-mode payload segments above 1024 items) are NOT sorted: they are
+ * counted in the workspace, and nsg_segments_check(ws) (which synchronises
+ * the stream) reports them as NSG_ERR_SPEC. */
 size_t nsg_segments_ws_bytes(int64_t nseg, int64_t nelem);
 int nsg_sort_segments(const nsg_spec* sp, const uint32_t* offsets, int64_t nseg, const void* keys_in,
                       void* keys_out, const void* pay_in, void* pay_out, void* ws, size_t ws_bytes, void* stream);

@@ -72,8 +72,8 @@ typedef struct {
  * (netsort_core.c:498-527).  `rows` is a DEVICE pointer to m*n packed
  * {uint64 key; uint64 ref} items (items.py:14), 16-byte aligned, sorted in
  * place row by row.  kind NETWORK: n in 2..16 (n < 2 is a no-op, else -2);
- * kind RSS: n <= 1024 (the reference's tie order, replayed draw for draw);
- * kind INSERTION: stable by key, n <= 1024. */
+ * kind RSS: any n (the reference's tie order, replayed draw for draw; above
+ * 1024 items in global memory); kind INSERTION: stable by key, any n. */
 int nsg_run_sorter_many(const nsg_spec* sp, void* rows, int64_t m, int64_t n, void* stream);
 
 /* Same with HOST rows (pinned memory overlaps copies with sorting). */
@@ -81,10 +81,11 @@ int nsg_run_sorter_many_host(const nsg_spec* sp, void* rows, int64_t m, int64_t 
 
 /* Typed SoA batch: `rows` rows of n keys (key_dtype) and optional payloads
  * (payload_dtype), row-major, device pointers, 16-byte aligned.  Out-of-place
- * or in-place (out == in).  Network kinds: n 1..16.  RSS and MERGE kinds,
- * keys-only or UNIQUE: any n (n > 1024 through a CTA sorter; above its
- * shared-memory capacity it allocates a stream-ordered scratch).  RSS with
- * REF-mode payload order and INSERTION: n <= 1024. */
+ * or in-place (out == in).  Network kinds: n 1..16.  RSS, MERGE and INSERTION
+ * kinds: any n (above 1024 items a stream-ordered scratch may be allocated:
+ * keys-only / UNIQUE rows take a CTA sorter, REF-mode payload order the
+ * reference recursion replayed in global memory).  MERGE requires UNIQUE
+ * with a payload. */
 int nsg_sort_rows(const nsg_spec* sp, const void* keys_in, void* keys_out, const void* pay_in, void* pay_out,
                   int64_t rows, int64_t n, void* stream);
 

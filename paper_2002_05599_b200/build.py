@@ -29,7 +29,7 @@ FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--
 def _units() -> list:
     """(object name, source, extra defines)"""
     units = [("net_n%02d.o" % n, CSRC / "net_sort_inst.cu", ["-DNSG_N=%d" % n]) for n in range(0, 17)]
-    for name in ("capi", "misc", "rss", "pksort", "bigsort", "netbulk", "nettma", "segments", "wmerge", "verify", "lane"):
+    for name in ("capi", "misc", "rss", "pksort", "bigsort", "netbulk", "nettma", "rssbig", "segments", "wmerge", "verify", "lane"):
         units.append((name + ".o", CSRC / (name + ".cu"), []))
     return units
 

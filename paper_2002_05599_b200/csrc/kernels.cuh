@@ -62,6 +62,12 @@ bool nettma_covers(int n, int key_bytes, int pay);
 int launch_nettma(int dag, int pay, int mode, const void* k_in, void* k_out, const void* p_in, void* p_out,
                   int64_t rows, const Xform& xf, cudaStream_t st);
 
+// rssbig.cu (the reference's RSS / insertion tie order above 1024 items,
+// one warp per row in global memory)
+int launch_rssbig_items(const nsg_spec& sp, void* rows, int64_t m, int64_t n, cudaStream_t st);
+int launch_rssbig_rows(const nsg_spec& sp, const void* k_in, void* k_out, const void* p_in, void* p_out,
+                       int64_t rows, int64_t n, int key_bytes, int pay, const Xform& xf, cudaStream_t st);
+
 // wmerge.cu
 int launch_wmerge(const nsg_spec& sp, const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows,
                   int64_t n, cudaStream_t st);

@@ -997,11 +997,23 @@ int launch_rss(const nsg_spec& sp, const void* k_in, void* k_out, const void* p_
                const uint32_t* seg_count = nullptr, uint32_t* seg_overflow = nullptr) {
   if (n > 1024 && !seg_ids) {
     // keys-only / UNIQUE rows: the output is the unique sorted order -- CTA
-    // sorter (bigsort.cu); REF-mode payload order above 1024 is not replayed
-    if (layout == LAYOUT_SOA && (pay == 0 || mode == MODE_UNIQUE))
+    // sorter (bigsort.cu); the reference's tie order (REF mode with payloads,
+    // AoS items, insertion kind): the recursion replayed in global memory
+    // (rssbig.cu)
+    if (sp.kind == NSG_KIND_RSS && layout == LAYOUT_SOA && (pay == 0 || mode == MODE_UNIQUE))
       return launch_bigsort_rows(k_in, k_out, p_in, p_out, rows, n, key_bytes, pay, xf, st);
-    return fail(NSG_ERR_SPEC, "RSS with reference tie order (REF mode, payload) is limited to 1024 items on the "
-                "device, got %lld", (long long)n);
+    if (sp.kind == NSG_KIND_RSS || sp.kind == NSG_KIND_INSERTION) {
+      if (sp.kind == NSG_KIND_RSS) {
+        if (sp.rss_oversampling < 1 || sp.rss_oversampling > 16)
+          return fail(NSG_ERR_SPEC, "RSS oversampling %d not in 1..16", sp.rss_oversampling);
+        if (sp.rss_threshold < 2) return fail(NSG_ERR_SPEC, "RSS threshold must be >= 2");
+        if (sp.base_kind == 0 && sp.rss_threshold > 16)
+          return fail(NSG_ERR_SPEC, "network base case caps the threshold at 16");
+      }
+      if (layout == LAYOUT_AOS16) return launch_rssbig_items(sp, k_out, rows, n, st);
+      if (pay == 0) return launch_bigsort_rows(k_in, k_out, p_in, p_out, rows, n, key_bytes, pay, xf, st);
+      return launch_rssbig_rows(sp, k_in, k_out, p_in, p_out, rows, n, key_bytes, pay, xf, st);
+    }
   }
   if (sp.kind == NSG_KIND_RSS) {
     if (sp.rss_oversampling < 1 || sp.rss_oversampling > 16)

@@ -56,12 +56,9 @@ def test_error_mapping(torch):
         smallsort.sort_small(items_from_keys(range(20)), 17, "SN Best 4CmS")
     with pytest.raises(UnsupportedSize):
         smallsort.sort_small(items_from_keys([3, 2, 1]), 3, "RSS 332 IS Def")
-    # RSS above 1024 items: keys-only sorts (CTA sorter), REF-mode payload order refuses
+    # RSS above 1024 items (no size cap, as the reference): keys-only through the CTA sorter
     k, _ = batch.sort_rows(np.arange(2200, dtype=np.uint64)[::-1].reshape(2, 1100).copy(), kind="rss")
     assert np.array_equal(k, np.sort(np.arange(2200, dtype=np.uint64)[::-1].reshape(2, 1100), axis=1))
-    with pytest.raises(ConfigurationError):
-        batch.sort_rows(np.zeros((2, 1100), dtype=np.uint64), np.zeros((2, 1100), dtype=np.uint64), kind="rss",
-                        tie="ref")
 
 
 def test_sort_small_dispatch_and_insertion(torch):

@@ -103,11 +103,65 @@ def test_big_rows_in_place(torch):
     assert np.array_equal(t.cpu().numpy(), np.sort(keys, axis=1))
 
 
-def test_big_rows_ref_payload_rejected(torch):
-    """REF-mode payload order (the reference's RSS replay) is not reproduced
-    above 1024 items: the call refuses instead of returning another order."""
-    from paper_2002_05599_b200 import batch
-    from paper_2002_05599_b200.errors import ConfigurationError
-    keys = np.zeros((2, 1025), dtype=np.uint64)
-    with pytest.raises(ConfigurationError):
-        batch.sort_rows(_t(torch, keys), _t(torch, keys), kind="rss", tie="ref")
+def _items(keys, refs):
+    it = np.empty(keys.shape, dtype=oracle.ITEM)
+    it["key"] = keys
+    it["ref"] = refs
+    return it
+
+
+@pytest.mark.parametrize("cfg,base", [("332", "SN Best 4CmS"), ("315", "SN BN-R TCOp"), ("391", "IS Def")])
+@pytest.mark.parametrize("n", [1025, 4096, 30000])
+def test_big_rows_ref_mode_rss_vs_oracle(cfg, base, n, torch):
+    """The reference's tie order above 1024 items (csrc/rssbig.cu): AoS items
+    through run_sorter_many, duplicate-heavy keys so the payload order under
+    ties shows every draw, bucket and base case."""
+    from paper_2002_05599_b200 import backend, registry
+    rng = np.random.default_rng(n + int(cfg))
+    spec = registry.spec_rss(cfg, base)
+    fam = "best" if "Best" in base or base.startswith("IS") else "bn-r"
+    kind_base = "ins" if base.startswith("IS") else "net"
+    m = 3
+    keys = rng.integers(0, 40, size=(m, n), dtype=np.uint64)
+    keys[1] = rng.integers(0, 2**64, size=n, dtype=np.uint64)  # distinct
+    keys[2, : n // 2] = 7                                     # one huge run of ties
+    refs = np.arange(m * n, dtype=np.uint64).reshape(m, n)
+    exp = _items(keys, refs)
+    oracle.run_items(exp, kind="rss", family=fam, rss_cfg=cfg, base=kind_base)
+    got = _items(keys, refs)
+    backend.run_sorter_many(spec, got)
+    assert np.array_equal(got, exp), (cfg, base, n)
+
+
+def test_big_rows_rss_sort_and_typed_ref(torch):
+    """rss.rss_sort (the reference's API, no size cap) and typed REF-mode rows
+    with a payload above 1024 items equal the oracle."""
+    from paper_2002_05599_b200 import batch, rss
+    from paper_2002_05599_b200.items import items_from_pairs
+    rng = np.random.default_rng(5)
+    keys = rng.integers(0, 9, size=3000, dtype=np.uint64)
+    arr = items_from_pairs(zip(keys.tolist(), range(3000)))
+    rss.rss_sort(arr, rss.RssConfig.from_string("332"))
+    exp = _items(keys.reshape(1, -1), np.arange(3000, dtype=np.uint64).reshape(1, -1))
+    oracle.run_items(exp, kind="rss", family="best", rss_cfg="332")
+    assert np.array_equal(arr, exp[0])
+    for kdt in ("int64", "uint32", "float32"):
+        k = rng.integers(-5, 5, size=(2, 2500)).astype(kdt)
+        pay = rng.integers(0, 2**31, size=(2, 2500)).astype(np.uint32)
+        for desc in (False, True):
+            ek, ep = oracle.typed_sort_rows(k, pay, descending=desc, unique=False, kind="rss")
+            gk, gp = batch.sort_rows(_t(torch, k), _t(torch, pay), kind="rss", tie="ref", descending=desc)
+            assert np.array_equal(gk.cpu().numpy().view(k.dtype), ek) and np.array_equal(gp.cpu().numpy(), ep), \
+                (kdt, desc)
+
+
+def test_big_rows_insertion_kind_is_stable(torch):
+    from paper_2002_05599_b200 import backend, registry
+    rng = np.random.default_rng(9)
+    keys = rng.integers(0, 6, size=(2, 2000), dtype=np.uint64)
+    refs = np.arange(4000, dtype=np.uint64).reshape(2, 2000)
+    got = _items(keys, refs)
+    backend.run_sorter_many(registry.spec_insertion("Def"), got)
+    for r in range(2):
+        o = np.argsort(keys[r], kind="stable")
+        assert np.array_equal(got[r]["key"], keys[r][o]) and np.array_equal(got[r]["ref"], refs[r][o])

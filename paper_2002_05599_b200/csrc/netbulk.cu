@@ -1,4 +1,4 @@
-// Network sort of odd-width rows (u64 keys, n = 9..15) staged by TMA bulk
+// Network sort of odd-width rows (u64 keys, n = 5, 9..15) staged by TMA bulk
 // copies: thread per row, warp-owned ring of row groups.
 //
 // Rows of an odd number of 8-byte keys (and of 4-byte payloads) are not
@@ -23,18 +23,20 @@ namespace nsg {
 
 namespace {
 
-// Two measured configurations (tools/nb_variants.py, profiles/round2/netbulk.md):
+// Three measured configurations (tools/nb_variants.py, profiles/round2/netbulk.md):
 //   A: 2 rows per lane, 48 KiB ring per warp, 4-warp CTAs (one per SM) --
 //      network-light shapes, where ring depth is what counts;
 //   B: 1 row per lane, 16 KiB ring, 8-warp CTAs -- u64 + u32 lexicographic
-//      n = 13 / 15, whose long compare-exchange chains want more warps.
+//      n = 13 / 15, whose long compare-exchange chains want more warps;
+//   C: 4 rows per lane, 56 KiB ring, 4-warp CTAs -- keys-only n = 5 (40-byte
+//      rows: small groups need a deeper ring to keep enough bytes in flight).
 template <int APL_, int RING_, int WARPS_>
 struct NbKnobs {
   static constexpr int APL = APL_, RING = RING_, WARPS = WARPS_;
 };
 using NbA = NbKnobs<2, 49152, 4>;
 using NbB = NbKnobs<1, 16384, 8>;
-using NbC = NbKnobs<4, 57344, 4>;  // short rows: bigger groups, deeper ring (tuning: NSG_NB_FORCE=3)
+using NbC = NbKnobs<4, 57344, 4>;  // keys-only n = 5 and BN n = 13: bigger groups, deeper ring
 
 template <int N, class U, class P, class K>
 struct NbCfg {
@@ -45,7 +47,7 @@ struct NbCfg {
   static constexpr int KB = ROWS * N * int(sizeof(U));
   static constexpr int PBB = ROWS * N * PB;
   static constexpr int NB_RAW = K::RING / (KB + PBB);
-  static constexpr int NB = NB_RAW < 3 ? 3 : NB_RAW > 8 ? 8 : NB_RAW;
+  static constexpr int NB = NB_RAW < 3 ? 3 : NB_RAW > 16 ? 16 : NB_RAW;
   static constexpr int AHEAD = NB - 2;
   static constexpr int OFF_P = NB * KB;
   static constexpr int OFF_BAR = (OFF_P + NB * PBB + 7) / 8 * 8;
@@ -194,9 +196,9 @@ NbLaunch nb_mode(int mode) {
 }
 
 // measured per shape (u64 keys; tools/nb_variants.py): 0 = the cp.async tile
-// kernel of net_sort.cuh stays faster, 1 = configuration A, 2 = B
+// kernel of net_sort.cuh stays faster, 1 = configuration A, 2 = B, 3 = C
 constexpr int nb_choice(int n, int dag, int pay) {
-  if (pay == 0) return (n == 11 || n == 13 || (n == 15 && dag == 0)) ? 1 : 0;
+  if (pay == 0) return n == 5 || (n == 13 && dag == 1) ? 3 : (n == 11 || n == 13 || (n == 15 && dag == 0)) ? 1 : 0;
   if (n == 9 || n == 11) return 1;
   if ((n == 13 && dag == 0) || n == 15) return 2;
   return 0;
@@ -233,7 +235,6 @@ NbLaunch nb_dag(int dag, int pay, int mode) {
 NbLaunch nb_lookup(int n, int dag, int pay, int mode) {
   switch (n) {
     case 5: return nb_dag<5>(dag, pay, mode);
-    case 7: return nb_dag<7>(dag, pay, mode);
     case 9: return nb_dag<9>(dag, pay, mode);
     case 11: return nb_dag<11>(dag, pay, mode);
     case 13: return nb_dag<13>(dag, pay, mode);
@@ -247,7 +248,7 @@ NbLaunch nb_lookup(int n, int dag, int pay, int mode) {
 // u64 keys (+ u32 payload), SoA, the odd widths where the bulk-staged kernel
 // measured faster than the cp.async tile pipeline
 bool netbulk_covers(int n, int dag, int key_bytes, int pay) {
-  return key_bytes == 8 && (pay == 0 || pay == 1) && (n & 1) && n >= 5 && n <= 15 &&
+  return key_bytes == 8 && (pay == 0 || pay == 1) && (n & 1) && n >= 5 && n <= 15 && n != 7 &&
          (nb_force() != 0 || nb_choice(n, dag ? 1 : 0, pay) != 0);
 }
 

@@ -359,12 +359,23 @@ struct PhaseRss {
       }
     }
     // ---- classify: binary search over the row's L-1 splitters ---------------
+    // the first two levels compare against three splitters every word of the
+    // row shares: fetched once per row, then selected in registers
+    const int rb = g << LOGL;  // lane of the row's first bucket
+    const uint32_t t_mid = __shfl_sync(0xffffffffu, s, rb + L / 2 - 1);
+    const uint32_t t_lo = L >= 4 ? __shfl_sync(0xffffffffu, s, rb + L / 4 - 1) : 0u;
+    const uint32_t t_hi = L >= 4 ? __shfl_sync(0xffffffffu, s, rb + L / 2 + L / 4 - 1) : 0u;
     int q[E];
 #pragma unroll
     for (int r = 0; r < E; ++r) {
-      int b = g << LOGL;  // lane of the row's first bucket
+      const bool c1 = t_mid < pk[r];
+      int b = rb | (c1 ? L / 2 : 0);
+      if constexpr (L >= 4) {
+        const bool c2 = (c1 ? t_hi : t_lo) < pk[r];
+        b |= c2 ? L / 4 : 0;
+      }
 #pragma unroll
-      for (int step = L / 2; step >= 1; step >>= 1) {
+      for (int step = L / 8; step >= 1; step >>= 1) {
         const uint32_t t = __shfl_sync(0xffffffffu, s, b + step - 1);
         b |= t < pk[r] ? step : 0;
       }

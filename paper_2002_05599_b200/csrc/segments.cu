@@ -309,6 +309,17 @@ __device__ __forceinline__ void sort_segment_padm(U* keys, P* pays, int len, con
 #ifndef NSG_SEG_PAD8
 #define NSG_SEG_PAD8 1
 #endif
+// Unique-order modes: one padded network per 32-segment chunk (the class of
+// its longest segment) instead of per-lane dispatch on the exact length.
+#ifndef NSG_SEG_UNIFORM
+#define NSG_SEG_UNIFORM 1
+#endif
+#ifndef NSG_SEG_U9
+#define NSG_SEG_U9 1   // 9-item class of its own (else padded to 10)
+#endif
+#ifndef NSG_SEG_U23
+#define NSG_SEG_U23 1  // 2- and 3-item classes of their own (else padded to 4)
+#endif
 
 template <class U, class P, int DAG, class CX, int XK>
 __device__ __forceinline__ void sort_segment_smem(U* keys, P* pays, int len, const Xform& xf) {
@@ -477,7 +488,28 @@ __global__ void __launch_bounds__(kThreads, NSG_SEG_MINB) seg_kernel(const SegPa
         const int c = k * NW + ((k & 1) ? (NW - 1 - w) : w);
         if (c >= nchunks) continue;
         const int j = c * 32 + lane;
-        if (j < nshort) {
+        if constexpr (NSG_SEG_UNIFORM && !std::is_same<CX, CxRef>::value) {
+          // unique-order modes: the whole chunk runs ONE padded network, the
+          // class of its longest segment (lane 0: perm is longest first), so a
+          // chunk that straddles two length classes does not execute both bodies
+          int st = 0, len = 0;
+          if (j < nshort) {
+            const int s = a + perm[j];
+            st = int(offs[s] - e0);
+            len = int(offs[s + 1] - offs[s]);
+            NSG_DCHECK(st >= 0 && int(offs[s + 1] - e0) <= G::CAP);
+          }
+          const int lmax = __shfl_sync(0xffffffffu, len, 0);
+          U* kp = reinterpret_cast<U*>(kb) + st;
+          P* pp = reinterpret_cast<P*>(pb) + st;
+          if (lmax > 10) sort_segment_padm<16, U, P, DAG, CX, XK>(kp, pp, len, xf);
+          else if (lmax == 10 || (!NSG_SEG_U9 && lmax == 9)) sort_segment_padm<10, U, P, DAG, CX, XK>(kp, pp, len, xf);
+          else if (NSG_SEG_U9 && lmax == 9) sort_segment_padm<9, U, P, DAG, CX, XK>(kp, pp, len, xf);
+          else if (lmax > 4) sort_segment_padm<8, U, P, DAG, CX, XK>(kp, pp, len, xf);
+          else if (lmax == 4 || !NSG_SEG_U23) sort_segment_padm<4, U, P, DAG, CX, XK>(kp, pp, len, xf);
+          else if (lmax == 3) sort_segment_padm<3, U, P, DAG, CX, XK>(kp, pp, len, xf);
+          else sort_segment_padm<2, U, P, DAG, CX, XK>(kp, pp, len, xf);
+        } else if (j < nshort) {
           const int s = a + perm[j];
           const int st = int(offs[s] - e0);
           NSG_DCHECK(st >= 0 && int(offs[s + 1] - e0) <= G::CAP);

@@ -51,6 +51,11 @@ namespace {
 #ifndef NSG_SEG_MINB
 #define NSG_SEG_MINB 2
 #endif
+// perm entries carry (first item << 5 | length), so the sort phase reads one
+// word per segment instead of the permutation and two offsets
+#ifndef NSG_SEG_PERM32
+#define NSG_SEG_PERM32 1
+#endif
 constexpr int kMaxTileSegs = NSG_SEG_TILE;
 constexpr int kThreads = NSG_SEG_THREADS;
 constexpr int kBufBytes = NSG_SEG_BUF_KB * 1024;  // one staging buffer (keys + payload regions)
@@ -83,8 +88,8 @@ struct SegGeom {
   static constexpr int TS_ = TS;
   static constexpr int OFFS_STRIDE = TS_ + 4;                    // u32 per offsets slot
   static constexpr int OFF_OFFS = 0;                                   // 3 slots
-  static constexpr int OFF_PERM = OFF_OFFS + 3 * OFFS_STRIDE * 4;      // TS_ u16
-  static constexpr int OFF_HIST = OFF_PERM + TS_ * 2;            // 32 int
+  static constexpr int OFF_PERM = OFF_OFFS + 3 * OFFS_STRIDE * 4;      // TS_ u16 (u32 with NSG_SEG_PERM32)
+  static constexpr int OFF_HIST = OFF_PERM + TS_ * (NSG_SEG_PERM32 ? 4 : 2);  // 32 int
   static constexpr int OFF_BAR = (OFF_HIST + 32 * 4 + 7) / 8 * 8;        // 2 mbarriers (bulk tile loads)
   static constexpr int OFF_DATA = (OFF_BAR + 2 * 8 + 15) / 16 * 16;       // 2 buffers
   static constexpr int SMEM = OFF_DATA + 2 * BUF;
@@ -201,6 +206,54 @@ __device__ __forceinline__ void store_range_bulk(const unsigned char* sm, T* dst
   if (tid == 0 && t_beg > h_end) bulk_s2g(g + h_end, sm + (h_end - base), unsigned(t_beg - h_end));
 }
 
+// Descending float keys (XK_FDESC) sort in the ASCENDING ordered space with the
+// comparator's operands swapped: the network then leaves the largest item in
+// channel 0, which is the descending (key, payload) order, and the payload
+// needs no transform at all (the descending payload order comes from the
+// swapped operands too).  Padding sentinels are the smallest item (0, 0).
+#ifndef NSG_SEG_REV
+#define NSG_SEG_REV 1
+#endif
+template <class CX>
+struct CxRev {
+  template <class E>
+  __device__ __forceinline__ static void cx(E& a, E& b) { CX::cx(b, a); }
+};
+template <class CX> struct IsRefCx { static constexpr bool value = false; };
+template <> struct IsRefCx<CxRef> { static constexpr bool value = true; };
+template <> struct IsRefCx<CxRev<CxRef>> { static constexpr bool value = true; };
+// float <-> ascending ordered space, one SHF + one LOP3 each way
+__device__ __forceinline__ uint32_t lop3_xor_or(uint32_t a, uint32_t b, uint32_t c) {  // a ^ (b | c)
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0x1e;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+__device__ __forceinline__ uint32_t lop3_xor_nor(uint32_t a, uint32_t b, uint32_t c) {  // a ^ (~b | c)
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0x4b;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+template <class U>
+__device__ __forceinline__ U fasc_to(U x) {
+  if constexpr (sizeof(U) == 4) {
+    return lop3_xor_or(x, uint32_t(int32_t(x) >> 31), 0x80000000u);
+  } else {
+    const uint32_t lo = uint32_t(x), hi = uint32_t(x >> 32);
+    const uint32_t s = uint32_t(int32_t(hi) >> 31);
+    return (uint64_t(lop3_xor_or(hi, s, 0x80000000u)) << 32) | (lo ^ s);
+  }
+}
+template <class U>
+__device__ __forceinline__ U fasc_from(U y) {
+  if constexpr (sizeof(U) == 4) {
+    return lop3_xor_nor(y, uint32_t(int32_t(y) >> 31), 0x80000000u);
+  } else {
+    const uint32_t lo = uint32_t(y), hi = uint32_t(y >> 32);
+    const uint32_t s = uint32_t(int32_t(hi) >> 31);
+    return (uint64_t(lop3_xor_nor(hi, s, 0x80000000u)) << 32) | (lo ^ ~s);
+  }
+}
+
 // Order transform kinds (template XK): none, generic, float descending.  The
 // transform is applied in registers around each network and nowhere else:
 // elements of single-item segments are staged and stored untouched, which is
@@ -210,19 +263,25 @@ enum { XK_NONE = 0, XK_GEN = 1, XK_FDESC = 2 };
 template <int XK, class U>
 __device__ __forceinline__ U xk_to(U k, const Xform& xf) {
   if constexpr (XK == XK_GEN) return to_ord<U>(k, xf);
-  else if constexpr (XK == XK_FDESC) return fdesc_ord<U>(k);
+  else if constexpr (XK == XK_FDESC) return NSG_SEG_REV ? fasc_to<U>(k) : fdesc_ord<U>(k);
   else return k;
 }
 template <int XK, class U>
 __device__ __forceinline__ U xk_from(U k, const Xform& xf) {
   if constexpr (XK == XK_GEN) return from_ord<U>(k, xf);
-  else if constexpr (XK == XK_FDESC) return fdesc_ord<U>(k);
+  else if constexpr (XK == XK_FDESC) return NSG_SEG_REV ? fasc_from<U>(k) : fdesc_ord<U>(k);
   else return k;
 }
 template <int XK, class P>
 __device__ __forceinline__ P xk_pay(P q, const Xform& xf) {
-  if constexpr (XK == XK_NONE) return q;
+  if constexpr (XK == XK_NONE || (XK == XK_FDESC && NSG_SEG_REV)) return q;
   else return P(q ^ P(xf.pdesc));
+}
+// padding sentinel: sorts last (the largest item, or the smallest under CxRev)
+template <int XK, class T>
+__device__ __forceinline__ T xk_pad() {
+  if constexpr (XK == XK_FDESC && NSG_SEG_REV) return T(0);
+  else return T(~T(0));
 }
 
 // One segment of exactly L items: load (into the ordered space), network,
@@ -262,8 +321,8 @@ __device__ __forceinline__ void sort_segment_pad16(U* keys, P* pays, int len, co
       v[j].k = xk_to<XK>(keys[j], xf);
       if constexpr (HAS_P) v[j].p = xk_pay<XK>(pays[j], xf);
     } else {
-      v[j].k = U(~U(0));
-      if constexpr (HAS_P) v[j].p = P(~P(0));
+      v[j].k = xk_pad<XK, U>();
+      if constexpr (HAS_P) v[j].p = xk_pad<XK, P>();
     }
   }
   Net<DAG, 16>::template run<CX>(v);
@@ -288,8 +347,8 @@ __device__ __forceinline__ void sort_segment_padm(U* keys, P* pays, int len, con
       v[j].k = xk_to<XK>(keys[j], xf);
       if constexpr (HAS_P) v[j].p = xk_pay<XK>(pays[j], xf);
     } else {
-      v[j].k = U(~U(0));
-      if constexpr (HAS_P) v[j].p = P(~P(0));
+      v[j].k = xk_pad<XK, U>();
+      if constexpr (HAS_P) v[j].p = xk_pad<XK, P>();
     }
   }
   Net<DAG, M>::template run<CX>(v);
@@ -317,14 +376,20 @@ __device__ __forceinline__ void sort_segment_padm(U* keys, P* pays, int len, con
 #ifndef NSG_SEG_U9
 #define NSG_SEG_U9 1   // 9-item class of its own (else padded to 10)
 #endif
+#ifndef NSG_SEG_U6
+#define NSG_SEG_U6 1   // 5..6 items through the 6-network (else padded to 8)
+#endif
+#ifndef NSG_SEG_U12
+#define NSG_SEG_U12 0  // 11..12 items through the 12-network: measured slower (cfg4 1.118 -> 1.148 ms)
+#endif
 #ifndef NSG_SEG_U23
 #define NSG_SEG_U23 1  // 2- and 3-item classes of their own (else padded to 4)
 #endif
 
 template <class U, class P, int DAG, class CX, int XK>
 __device__ __forceinline__ void sort_segment_smem(U* keys, P* pays, int len, const Xform& xf) {
-  constexpr bool kPad16 = DAG == 0 || !std::is_same<CX, CxRef>::value;
-  if constexpr (NSG_SEG_PAD8 && !std::is_same<CX, CxRef>::value) {
+  constexpr bool kPad16 = DAG == 0 || !IsRefCx<CX>::value;
+  if constexpr (NSG_SEG_PAD8 && !IsRefCx<CX>::value) {
     if (len >= 5 && len <= 8) {
       sort_segment_padm<8, U, P, DAG, CX, XK>(keys, pays, len, xf);
       return;
@@ -366,11 +431,13 @@ template <class U, class P, int MODE, int DAG, int XK>
 __global__ void __launch_bounds__(kThreads, NSG_SEG_MINB) seg_kernel(const SegParams prm) {
   using G = SegGeom<U, P>;
   constexpr bool HAS_P = !IsNoPay<P>::value;
-  using CX = typename std::conditional<!HAS_P, CxKeys,
-                                       typename std::conditional<MODE == MODE_REF, CxRef, CxUnique>::type>::type;
+  using CXA = typename std::conditional<!HAS_P, CxKeys,
+                                        typename std::conditional<MODE == MODE_REF, CxRef, CxUnique>::type>::type;
+  using CX = typename std::conditional<XK == XK_FDESC && NSG_SEG_REV, CxRev<CXA>, CXA>::type;
   constexpr int TS_ = G::TS;
   extern __shared__ __align__(16) unsigned char sm[];
-  uint16_t* perm = reinterpret_cast<uint16_t*>(sm + G::OFF_PERM);
+  using PermT = typename std::conditional<NSG_SEG_PERM32 != 0, uint32_t, uint16_t>::type;
+  PermT* perm = reinterpret_cast<PermT*>(sm + G::OFF_PERM);
   int* hist = reinterpret_cast<int*>(sm + G::OFF_HIST);
   const int tid = threadIdx.x;
   const Xform xf = prm.xf;
@@ -439,12 +506,15 @@ __global__ void __launch_bounds__(kThreads, NSG_SEG_MINB) seg_kernel(const SegPa
     // length bin is kept in registers and placed after the scan
     constexpr int SPT = (TS_ + kThreads - 1) / kThreads;
     int lens[SPT], ranks[SPT];
+    [[maybe_unused]] uint32_t sts[SPT];
 #pragma unroll
     for (int i = 0; i < SPT; ++i) {
       const int s = a + tid + i * kThreads;
       lens[i] = 0;
       if (s < b) {
-        const int len = int(offs[s + 1] - offs[s]);
+        const uint32_t o0 = offs[s];
+        const int len = int(offs[s + 1] - o0);
+        if constexpr (NSG_SEG_PERM32) sts[i] = o0 - e0;
         if (len > 16) {
           const uint32_t slot = atomicAdd(prm.long_count, 1u);
           if (slot < prm.long_cap)
@@ -473,7 +543,11 @@ __global__ void __launch_bounds__(kThreads, NSG_SEG_MINB) seg_kernel(const SegPa
 #pragma unroll
     for (int i = 0; i < SPT; ++i) {
       const int start = __shfl_sync(0xffffffffu, excl, (16 - lens[i]) & 31);
-      if (lens[i]) perm[start + ranks[i]] = uint16_t(tid + i * kThreads);
+      if constexpr (NSG_SEG_PERM32) {
+        if (lens[i]) perm[start + ranks[i]] = (sts[i] << 5) | uint32_t(lens[i]);
+      } else {
+        if (lens[i]) perm[start + ranks[i]] = PermT(tid + i * kThreads);
+      }
     }
     __syncthreads();
     if (staged) {
@@ -488,12 +562,17 @@ __global__ void __launch_bounds__(kThreads, NSG_SEG_MINB) seg_kernel(const SegPa
         const int c = k * NW + ((k & 1) ? (NW - 1 - w) : w);
         if (c >= nchunks) continue;
         const int j = c * 32 + lane;
-        if constexpr (NSG_SEG_UNIFORM && !std::is_same<CX, CxRef>::value) {
+        if constexpr (NSG_SEG_UNIFORM && !IsRefCx<CX>::value) {
           // unique-order modes: the whole chunk runs ONE padded network, the
           // class of its longest segment (lane 0: perm is longest first), so a
           // chunk that straddles two length classes does not execute both bodies
           int st = 0, len = 0;
-          if (j < nshort) {
+          if constexpr (NSG_SEG_PERM32) {
+            const uint32_t pe = j < nshort ? perm[j] : 0u;
+            st = int(pe >> 5);
+            len = int(pe & 31u);
+            NSG_DCHECK(st >= 0 && st + len <= G::CAP);
+          } else if (j < nshort) {
             const int s = a + perm[j];
             st = int(offs[s] - e0);
             len = int(offs[s + 1] - offs[s]);
@@ -502,19 +581,28 @@ __global__ void __launch_bounds__(kThreads, NSG_SEG_MINB) seg_kernel(const SegPa
           const int lmax = __shfl_sync(0xffffffffu, len, 0);
           U* kp = reinterpret_cast<U*>(kb) + st;
           P* pp = reinterpret_cast<P*>(pb) + st;
-          if (lmax > 10) sort_segment_padm<16, U, P, DAG, CX, XK>(kp, pp, len, xf);
+          if (lmax > (NSG_SEG_U12 ? 12 : 10)) sort_segment_padm<16, U, P, DAG, CX, XK>(kp, pp, len, xf);
+          else if (NSG_SEG_U12 && lmax > 10) sort_segment_padm<12, U, P, DAG, CX, XK>(kp, pp, len, xf);
           else if (lmax == 10 || (!NSG_SEG_U9 && lmax == 9)) sort_segment_padm<10, U, P, DAG, CX, XK>(kp, pp, len, xf);
           else if (NSG_SEG_U9 && lmax == 9) sort_segment_padm<9, U, P, DAG, CX, XK>(kp, pp, len, xf);
-          else if (lmax > 4) sort_segment_padm<8, U, P, DAG, CX, XK>(kp, pp, len, xf);
+          else if (lmax > (NSG_SEG_U6 ? 6 : 4)) sort_segment_padm<8, U, P, DAG, CX, XK>(kp, pp, len, xf);
+          else if (NSG_SEG_U6 && lmax > 4) sort_segment_padm<6, U, P, DAG, CX, XK>(kp, pp, len, xf);
           else if (lmax == 4 || !NSG_SEG_U23) sort_segment_padm<4, U, P, DAG, CX, XK>(kp, pp, len, xf);
           else if (lmax == 3) sort_segment_padm<3, U, P, DAG, CX, XK>(kp, pp, len, xf);
           else sort_segment_padm<2, U, P, DAG, CX, XK>(kp, pp, len, xf);
         } else if (j < nshort) {
-          const int s = a + perm[j];
-          const int st = int(offs[s] - e0);
-          NSG_DCHECK(st >= 0 && int(offs[s + 1] - e0) <= G::CAP);
-          sort_segment_smem<U, P, DAG, CX, XK>(reinterpret_cast<U*>(kb) + st, reinterpret_cast<P*>(pb) + st,
-                                               int(offs[s + 1] - offs[s]), xf);
+          int st, len;
+          if constexpr (NSG_SEG_PERM32) {
+            const uint32_t pe = perm[j];
+            st = int(pe >> 5);
+            len = int(pe & 31u);
+          } else {
+            const int s = a + perm[j];
+            st = int(offs[s] - e0);
+            len = int(offs[s + 1] - offs[s]);
+          }
+          NSG_DCHECK(st >= 0 && st + len <= G::CAP);
+          sort_segment_smem<U, P, DAG, CX, XK>(reinterpret_cast<U*>(kb) + st, reinterpret_cast<P*>(pb) + st, len, xf);
         }
       }
     }

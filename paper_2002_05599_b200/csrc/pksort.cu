@@ -632,21 +632,32 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
     //         exactly (rare: distinct keys agreeing on every kept bit) ---------
     unsigned bad_rows = forced & ((rin >= 32 ? 0u : (1u << rin)) - 1u);
     if (tied) {
+      // branch-free: every lane loads its E predecessors back to back (the
+      // loads stay inside the buffer for every r; position 0 compares with
+      // itself) and the validity masks are applied to the predicate
       const U M = U(xf.sign_or ^ xf.kdesc);
-      auto kord = [&](U v) -> U { return xf.flt ? to_ord<U>(v, xf) : U(v ^ M); };
       bool bad = false;
+      auto check = [&](auto kord) {
 #pragma unroll
-      for (int r = 0; r < E; ++r) {
-        const int q = ll + L * r;
-        if ((FULL ? rowv : r < rl) && q > 0) {
+        for (int r = 0; r < E; ++r) {
+          const int q = ll + L * r;
+          const int qp = q - (q > 0 ? 1 : 0);
+          const U pk_ = rk[qp];
           P a{}, bq{};
           if constexpr (HAS_P) {
-            a = P(rp[q - 1] ^ P(xf.pdesc));
+            a = P(rp[qp] ^ P(xf.pdesc));
             bq = P(op[r] ^ P(xf.pdesc));
           }
-          bad |= item_lt<U, P>(kord(ok[r]), bq, kord(rk[q - 1]), a);
+          const bool lt = item_lt<U, P>(kord(ok[r]), bq, kord(pk_), a);
+          bad |= (FULL || r < rl) && lt;
         }
+      };
+      if (xf.flt) {
+        check([&](U v) -> U { return to_ord<U>(v, xf); });
+      } else {
+        check([&](U v) -> U { return U(v ^ M); });
       }
+      bad = bad && rowv;
       const unsigned bm = __ballot_sync(0xffffffffu, bad);
 #pragma unroll
       for (int gg = 0; gg < R; ++gg) {

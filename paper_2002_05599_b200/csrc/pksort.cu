@@ -314,6 +314,16 @@ struct PhaseBitonic {
   }
 };
 
+#ifndef NSG_RSS_NET_FMA
+#define NSG_RSS_NET_FMA 0  // base-case 8-network on CxFma
+#endif
+#ifndef NSG_RSS_RND_FMA
+#define NSG_RSS_RND_FMA 0  // merge-split role select as IMADs
+#endif
+#ifndef NSG_RSS_HC_FMA
+#define NSG_RSS_HC_FMA 0   // leading half-cleaner stages (of 3) of a merge-split round on CxFma
+#endif
+
 // Register Sample Sort, one level (north star (d); reference ns_rss_rec,
 // netsort_core.c:325-391): the row's L lanes draw one sample each at the
 // reference generator's positions (minstd, netsort_core.c:38-40), sort the
@@ -407,7 +417,8 @@ struct PhaseRss {
     // ---- base case: 8-word blocks, network, merge-split rounds ---------------
 #pragma unroll
     for (int r = 0; r < E; ++r) pk[r] = prow[ll * E + r];
-    Net<0, E>::template run_k<CxAlu>(pk, c.k);
+    using CXN = typename std::conditional<NSG_RSS_NET_FMA != 0, CxFma, CxAlu>::type;
+    Net<0, E>::template run_k<CXN>(pk, c.k);
     const int rounds = maxb <= 1u ? 0 : min(int(maxb - 2u) / E + 2, L);
     for (int t = 0; t < rounds; ++t) {
       // pairs (2m, 2m+1) on even rounds, (2m+1, 2m+2) on odd ones, inside the row
@@ -421,16 +432,36 @@ struct PhaseRss {
       uint32_t o[E];
 #pragma unroll
       for (int r = 0; r < E; ++r) o[r] = __shfl_sync(0xffffffffu, pk[E - 1 - r], src);
-#pragma unroll
-      for (int r = 0; r < E; ++r) {
-        const bool mn = r < E / 2 ? lo_half : hi_half;
-        pk[r] = mn ? min(pk[r], o[r]) : max(pk[r], o[r]);
-      }
-#pragma unroll
-      for (int j = E / 2; j > 0; j >>= 1) {
+      if constexpr (NSG_RSS_RND_FMA) {
+        // keep min or max by role without a select: with m = min(v, o) the
+        // result is m*c1 + (v + o)*c2, (c1, c2) = (1, 0) for the min and
+        // (-1, 1) for the max -- one VIMNMX and three IMADs (the FMA pipe is
+        // idle here, the ALU pipe the bottleneck)
+        const uint32_t c1l = lo_half ? c.k.one : c.k.neg1, c2l = lo_half ? 0u : c.k.one;
+        const uint32_t c1h = hi_half ? c.k.one : c.k.neg1, c2h = hi_half ? 0u : c.k.one;
 #pragma unroll
         for (int r = 0; r < E; ++r) {
-          if ((r & j) == 0) CxAlu::cx(pk[r], pk[r | j], c.k);
+          const uint32_t m = min(pk[r], o[r]);
+          const uint32_t sum = mad_lo(pk[r], c.k.one, o[r]);
+          const uint32_t u = mad_lo(sum, r < E / 2 ? c2l : c2h, 0u);
+          pk[r] = mad_lo(m, r < E / 2 ? c1l : c1h, u);
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          const bool mn = r < E / 2 ? lo_half : hi_half;
+          pk[r] = mn ? min(pk[r], o[r]) : max(pk[r], o[r]);
+        }
+      }
+      int stage = 0;
+#pragma unroll
+      for (int j = E / 2; j > 0; j >>= 1, ++stage) {
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          if ((r & j) == 0) {
+            if (stage < NSG_RSS_HC_FMA) CxFma::cx(pk[r], pk[r | j], c.k);
+            else CxAlu::cx(pk[r], pk[r | j], c.k);
+          }
         }
       }
     }

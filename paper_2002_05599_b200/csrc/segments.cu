@@ -382,6 +382,11 @@ __device__ __forceinline__ void sort_segment_padm(U* keys, P* pays, int len, con
 #ifndef NSG_SEG_U12
 #define NSG_SEG_U12 0  // 11..12 items through the 12-network: measured slower (cfg4 1.118 -> 1.148 ms)
 #endif
+// count the next tile's segments while this one is sorted, place them while
+// it is stored: two CTA barriers per tile instead of four
+#ifndef NSG_SEG_PIPE
+#define NSG_SEG_PIPE 1
+#endif
 #ifndef NSG_SEG_U23
 #define NSG_SEG_U23 1  // 2- and 3-item classes of their own (else padded to 4)
 #endif
@@ -495,18 +500,21 @@ __global__ void __launch_bounds__(kThreads, NSG_SEG_MINB) seg_kernel(const SegPa
     return true;
   };
 
-  // Bin + sort + store the segments [a, b) of a tile whose elements
-  // [offs[a], offs[b]) are staged in `buf` (or, if !staged, only collect longs).
-  auto process = [&](const uint32_t* offs, int a, int b, int64_t seg0, unsigned char* buf, bool staged) {
-    const uint32_t e0 = offs[a], e1 = offs[b];
-    unsigned char* kb = buf + range_shift<int(sizeof(U))>(e0);
-    unsigned char* pb = buf + G::K_REG + (HAS_P ? range_shift<G::PB>(e0) : 0);
-    // hist[] is zero here (prologue / previous call); callers synchronise first
-    // each thread bins its SPT segments; the rank atomicAdd returns inside a
-    // length bin is kept in registers and placed after the scan
-    constexpr int SPT = (TS_ + kThreads - 1) / kThreads;
-    int lens[SPT], ranks[SPT];
-    [[maybe_unused]] uint32_t sts[SPT];
+  // ---- the phases of one work item: segments [a, b) of a tile whose elements
+  // [offs[a], offs[b]) are staged in one buffer -------------------------------
+  // hist[] counts CUMULATIVELY over the CTA's life (never zeroed): each warp
+  // keeps the totals of the previous item in lane registers (hbase: lane l
+  // holds bin 16 - l) and works with the differences, so binning needs no
+  // reset pass and no barrier of its own.
+  constexpr int SPT = (TS_ + kThreads - 1) / kThreads;
+  constexpr int NW = kThreads / 32;
+  const int lane = tid & 31;
+  int hbase = 0;
+  // count: each thread bins its SPT segments; the (cumulative) rank the
+  // histogram atomic returns is kept in registers and placed after the scan
+  auto count = [&](const uint32_t* offs, int a, int b, int64_t seg0, int (&lens)[SPT], int (&ranks)[SPT],
+                   uint32_t (&sts)[SPT]) {
+    const uint32_t e0 = offs[a];
 #pragma unroll
     for (int i = 0; i < SPT; ++i) {
       const int s = a + tid + i * kThreads;
@@ -514,7 +522,7 @@ __global__ void __launch_bounds__(kThreads, NSG_SEG_MINB) seg_kernel(const SegPa
       if (s < b) {
         const uint32_t o0 = offs[s];
         const int len = int(offs[s + 1] - o0);
-        if constexpr (NSG_SEG_PERM32) sts[i] = o0 - e0;
+        sts[i] = o0 - e0;
         if (len > 16) {
           const uint32_t slot = atomicAdd(prm.long_count, 1u);
           if (slot < prm.long_cap)
@@ -527,95 +535,75 @@ __global__ void __launch_bounds__(kThreads, NSG_SEG_MINB) seg_kernel(const SegPa
         }
       }
     }
-    __syncthreads();
-    // every warp scans the 15 bin counts itself (exclusive, LONGEST first:
-    // lane l holds bin 16 - l), so no barrier separates scan and placement
-    const int lane = tid & 31;
-    const int v = lane < 15 ? hist[16 - lane] : 0;
+  };
+  // place (after a barrier that follows every thread's count): every warp scans
+  // the 15 bin counts itself (exclusive, LONGEST first), then each thread
+  // writes its segments' perm entries; returns the number of binned segments
+  auto place = [&](const int (&lens)[SPT], const int (&ranks)[SPT], const uint32_t (&sts)[SPT]) -> int {
+    const int h = lane < 15 ? hist[16 - lane] : 0;
+    const int v = h - hbase;
     int incl = v;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, incl, d);
-      if (lane >= d) incl += t;
+      const int t2 = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += t2;
     }
-    const int excl = incl - v;
+    const int sv = incl - v - hbase;  // bin start minus the bin's cumulative base
+    hbase = h;
     const int nshort = __shfl_sync(0xffffffffu, incl, 31);
 #pragma unroll
     for (int i = 0; i < SPT; ++i) {
-      const int start = __shfl_sync(0xffffffffu, excl, (16 - lens[i]) & 31);
+      const int start = __shfl_sync(0xffffffffu, sv, (16 - lens[i]) & 31);
       if constexpr (NSG_SEG_PERM32) {
         if (lens[i]) perm[start + ranks[i]] = (sts[i] << 5) | uint32_t(lens[i]);
       } else {
         if (lens[i]) perm[start + ranks[i]] = PermT(tid + i * kThreads);
       }
     }
-    __syncthreads();
-    if (staged) {
-      // 32-segment chunks in descending cost order are dealt to the warps in
-      // snake order (w, then 2W-1-w, ...): a static longest-first schedule, so
-      // the barrier after this loop waits for balanced work without a shared
-      // work counter
-      constexpr int NW = kThreads / 32;
-      const int w = tid >> 5;
-      const int nchunks = (nshort + 31) / 32;
-      for (int k = 0; k * NW < nchunks; ++k) {
-        const int c = k * NW + ((k & 1) ? (NW - 1 - w) : w);
-        if (c >= nchunks) continue;
-        const int j = c * 32 + lane;
-        if constexpr (NSG_SEG_UNIFORM && !IsRefCx<CX>::value) {
-          // unique-order modes: the whole chunk runs ONE padded network, the
-          // class of its longest segment (lane 0: perm is longest first), so a
-          // chunk that straddles two length classes does not execute both bodies
-          int st = 0, len = 0;
-          if constexpr (NSG_SEG_PERM32) {
-            const uint32_t pe = j < nshort ? perm[j] : 0u;
-            st = int(pe >> 5);
-            len = int(pe & 31u);
-            NSG_DCHECK(st >= 0 && st + len <= G::CAP);
-          } else if (j < nshort) {
-            const int s = a + perm[j];
-            st = int(offs[s] - e0);
-            len = int(offs[s + 1] - offs[s]);
-            NSG_DCHECK(st >= 0 && int(offs[s + 1] - e0) <= G::CAP);
-          }
-          const int lmax = __shfl_sync(0xffffffffu, len, 0);
-          U* kp = reinterpret_cast<U*>(kb) + st;
-          P* pp = reinterpret_cast<P*>(pb) + st;
-          if (lmax > (NSG_SEG_U12 ? 12 : 10)) sort_segment_padm<16, U, P, DAG, CX, XK>(kp, pp, len, xf);
-          else if (NSG_SEG_U12 && lmax > 10) sort_segment_padm<12, U, P, DAG, CX, XK>(kp, pp, len, xf);
-          else if (lmax == 10 || (!NSG_SEG_U9 && lmax == 9)) sort_segment_padm<10, U, P, DAG, CX, XK>(kp, pp, len, xf);
-          else if (NSG_SEG_U9 && lmax == 9) sort_segment_padm<9, U, P, DAG, CX, XK>(kp, pp, len, xf);
-          else if (lmax > (NSG_SEG_U6 ? 6 : 4)) sort_segment_padm<8, U, P, DAG, CX, XK>(kp, pp, len, xf);
-          else if (NSG_SEG_U6 && lmax > 4) sort_segment_padm<6, U, P, DAG, CX, XK>(kp, pp, len, xf);
-          else if (lmax == 4 || !NSG_SEG_U23) sort_segment_padm<4, U, P, DAG, CX, XK>(kp, pp, len, xf);
-          else if (lmax == 3) sort_segment_padm<3, U, P, DAG, CX, XK>(kp, pp, len, xf);
-          else sort_segment_padm<2, U, P, DAG, CX, XK>(kp, pp, len, xf);
-        } else if (j < nshort) {
-          int st, len;
-          if constexpr (NSG_SEG_PERM32) {
-            const uint32_t pe = perm[j];
-            st = int(pe >> 5);
-            len = int(pe & 31u);
-          } else {
-            const int s = a + perm[j];
-            st = int(offs[s] - e0);
-            len = int(offs[s + 1] - offs[s]);
-          }
-          NSG_DCHECK(st >= 0 && st + len <= G::CAP);
-          sort_segment_smem<U, P, DAG, CX, XK>(reinterpret_cast<U*>(kb) + st, reinterpret_cast<P*>(pb) + st, len, xf);
-        }
+    return nshort;
+  };
+  // sort: 32-segment chunks in descending cost order are dealt to the warps in
+  // snake order (w, then 2W-1-w, ...): a static longest-first schedule, so the
+  // barrier after it waits for balanced work without a shared work counter
+  auto sort_chunks = [&](const uint32_t* offs, int a, unsigned char* kb, unsigned char* pb, int nshort) {
+    const int w = tid >> 5;
+    const int nchunks = (nshort + 31) / 32;
+    [[maybe_unused]] const uint32_t e0 = offs[a];
+    for (int k = 0; k * NW < nchunks; ++k) {
+      const int c = k * NW + ((k & 1) ? (NW - 1 - w) : w);
+      if (c >= nchunks) continue;
+      const int j = c * 32 + lane;
+      int st = 0, len = 0;
+      if constexpr (NSG_SEG_PERM32) {
+        const uint32_t pe = j < nshort ? perm[j] : 0u;
+        st = int(pe >> 5);
+        len = int(pe & 31u);
+      } else if (j < nshort) {
+        const int s = a + perm[j];
+        st = int(offs[s] - e0);
+        len = int(offs[s + 1] - offs[s]);
+      }
+      NSG_DCHECK(st >= 0 && st + len <= G::CAP);
+      U* kp = reinterpret_cast<U*>(kb) + st;
+      P* pp = reinterpret_cast<P*>(pb) + st;
+      if constexpr (NSG_SEG_UNIFORM && !IsRefCx<CX>::value) {
+        // unique-order modes: the whole chunk runs ONE padded network, the
+        // class of its longest segment (lane 0: perm is longest first), so a
+        // chunk that straddles two length classes does not execute both bodies
+        const int lmax = __shfl_sync(0xffffffffu, len, 0);
+        if (lmax > (NSG_SEG_U12 ? 12 : 10)) sort_segment_padm<16, U, P, DAG, CX, XK>(kp, pp, len, xf);
+        else if (NSG_SEG_U12 && lmax > 10) sort_segment_padm<12, U, P, DAG, CX, XK>(kp, pp, len, xf);
+        else if (lmax == 10 || (!NSG_SEG_U9 && lmax == 9)) sort_segment_padm<10, U, P, DAG, CX, XK>(kp, pp, len, xf);
+        else if (NSG_SEG_U9 && lmax == 9) sort_segment_padm<9, U, P, DAG, CX, XK>(kp, pp, len, xf);
+        else if (lmax > (NSG_SEG_U6 ? 6 : 4)) sort_segment_padm<8, U, P, DAG, CX, XK>(kp, pp, len, xf);
+        else if (NSG_SEG_U6 && lmax > 4) sort_segment_padm<6, U, P, DAG, CX, XK>(kp, pp, len, xf);
+        else if (lmax == 4 || !NSG_SEG_U23) sort_segment_padm<4, U, P, DAG, CX, XK>(kp, pp, len, xf);
+        else if (lmax == 3) sort_segment_padm<3, U, P, DAG, CX, XK>(kp, pp, len, xf);
+        else sort_segment_padm<2, U, P, DAG, CX, XK>(kp, pp, len, xf);
+      } else if (j < nshort) {
+        sort_segment_smem<U, P, DAG, CX, XK>(kp, pp, len, xf);
       }
     }
-    // this thread's generic writes of `buf` before the copy engine reads it
-    fence_proxy_async_smem();
-    __syncthreads();
-    if (tid < 32) hist[tid] = 0;  // ready for the next call (after its leading sync)
-    if (staged) {  // (elements are back in their own representation)
-      store_range_bulk<U>(buf, kout, e0, e1, tid);
-      if constexpr (HAS_P) store_range_bulk<P>(buf + G::K_REG, pout, e0, e1, tid);
-      if (tid == 0) bulk_commit();
-    }
-    // no trailing barrier: the next tile starts with wait + __syncthreads
   };
 
   int t = int(blockIdx.x);
@@ -640,6 +628,18 @@ __global__ void __launch_bounds__(kThreads, NSG_SEG_MINB) seg_kernel(const SegPa
     if (t + gstride < ntiles) issue_offs(t + gstride, offs_slot(1));
     cp_async_commit();
   }
+  // Software pipeline over tiles: while tile k is sorted, the segments of tile
+  // k+1 are counted into the histogram (it needs only the offsets, which are
+  // two tiles ahead), and its perm entries are placed while tile k is stored --
+  // two CTA barriers per tile:
+  //   [A] data(k), offsets(k+1) and perm(k) visible
+  //        prefetch data(k+1) / offsets(k+2); count(k+1); sort(k)
+  //   [B] tile k sorted, histogram of k+1 complete
+  //        store(k); place(k+1)
+  bool binned = false;  // perm / nshort_cur already describe the current tile
+  int nshort_cur = 0;
+  int lens[SPT], ranks[SPT];
+  uint32_t sts[SPT];
   for (int k = 0; t < ntiles; ++k, t += gstride) {
     cp_async_wait<0>();
     if (bulk_pending & (1u << (k & 1))) {
@@ -647,24 +647,26 @@ __global__ void __launch_bounds__(kThreads, NSG_SEG_MINB) seg_kernel(const SegPa
       phases ^= 1u << (k & 1);
       bulk_pending &= ~(1u << (k & 1));
     }
-    __syncthreads();
+    __syncthreads();  // [A]
     const uint32_t* offs = offs_slot(k);
     const int nts = nsegs_of(t);
     const bool fits = offs[nts] - offs[0] <= uint32_t(G::CAP);
     const int tn = t + gstride;
+    const uint32_t* on = offs_slot(k + 1);
+    int ntn = 0;
+    bool next_fits = false;
     if (tn < ntiles) {  // prefetch: data of the next tile, offsets of the one after
-      const uint32_t* on = offs_slot(k + 1);
       if (tid == 0) bulk_wait_read<0>();  // the previous tile's bulk stores have read that slot
-      const int ntn = nsegs_of(tn);
-      if (on[ntn] - on[0] <= uint32_t(G::CAP) && issue_data_bulk(k + 1, on[0], on[ntn]))
-        bulk_pending |= 1u << ((k + 1) & 1);
+      ntn = nsegs_of(tn);
+      next_fits = on[ntn] - on[0] <= uint32_t(G::CAP);
+      if (next_fits && issue_data_bulk(k + 1, on[0], on[ntn])) bulk_pending |= 1u << ((k + 1) & 1);
       if (tn + gstride < ntiles) issue_offs(tn + gstride, offs_slot(k + 2));
     }
     cp_async_commit();
     unsigned char* buf = data_slot(k);
-    // a fitting tile is one prefetched sub-tile; an oversized one is cut into
-    // synchronous sub-tiles of <= CAP elements (one call site keeps `process`
-    // inlined, so the per-thread network stays in registers)
+    // a fitting tile is one prefetched item; an oversized one is cut into
+    // synchronous sub-tiles of <= CAP elements (one loop body, so the network
+    // code exists once)
     int a = 0;
     while (a < nts) {
       int b = nts;
@@ -690,7 +692,28 @@ __global__ void __launch_bounds__(kThreads, NSG_SEG_MINB) seg_kernel(const SegPa
         }
         __syncthreads();
       }
-      process(offs, a, b, int64_t(t) * TS_, buf, staged);
+      const uint32_t e0 = offs[a], e1 = offs[b];
+      unsigned char* kb = buf + range_shift<int(sizeof(U))>(e0);
+      unsigned char* pb = buf + G::K_REG + (HAS_P ? range_shift<G::PB>(e0) : 0);
+      if (!binned) {  // first tile, sub-tiles, the tile after an oversized one
+        count(offs, a, b, int64_t(t) * TS_, lens, ranks, sts);
+        __syncthreads();
+        nshort_cur = place(lens, ranks, sts);
+        __syncthreads();
+      }
+      const bool ahead = NSG_SEG_PIPE && fits && next_fits;
+      if (ahead) count(on, 0, ntn, int64_t(tn) * TS_, lens, ranks, sts);
+      if (staged) sort_chunks(offs, a, kb, pb, nshort_cur);
+      // this thread's generic writes of `buf` before the copy engine reads it
+      fence_proxy_async_smem();
+      __syncthreads();  // [B]
+      if (staged) {  // (elements are back in their own representation)
+        store_range_bulk<U>(buf, kout, e0, e1, tid);
+        if constexpr (HAS_P) store_range_bulk<P>(buf + G::K_REG, pout, e0, e1, tid);
+        if (tid == 0) bulk_commit();
+      }
+      if (ahead) nshort_cur = place(lens, ranks, sts);
+      binned = ahead;
       a = b;
     }
   }

@@ -315,13 +315,13 @@ struct PhaseBitonic {
 };
 
 #ifndef NSG_RSS_NET_FMA
-#define NSG_RSS_NET_FMA 0  // base-case 8-network on CxFma
+#define NSG_RSS_NET_FMA 1  // base-case 8-network on CxFma (n=256 uniform 1.522 -> 1.506 ms)
 #endif
 #ifndef NSG_RSS_RND_FMA
-#define NSG_RSS_RND_FMA 0  // merge-split role select as IMADs
+#define NSG_RSS_RND_FMA 0  // merge-split role select as IMADs: measured slower (1.59 -> 1.61 ms)
 #endif
 #ifndef NSG_RSS_HC_FMA
-#define NSG_RSS_HC_FMA 0   // leading half-cleaner stages (of 3) of a merge-split round on CxFma
+#define NSG_RSS_HC_FMA 3   // leading half-cleaner stages (of 3) of a merge-split round on CxFma (1.588 -> 1.522 ms)
 #endif
 
 // Register Sample Sort, one level (north star (d); reference ns_rss_rec,

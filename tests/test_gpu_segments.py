@@ -103,6 +103,30 @@ def test_segments_tile_overflow_split(torch):
     assert np.array_equal(gk, ek) and np.array_equal(gp, ep)
 
 
+@pytest.mark.parametrize("tie", ["unique", "ref"])
+def test_segments_pipeline_transitions(tie, torch):
+    """More tiles than CTAs, so every CTA walks several tiles and the
+    software pipeline (count tile k+1 while tile k sorts) runs; stretches of
+    16-item segments make some tiles exceed the staging buffer, so the kernel
+    moves between pipelined tiles and synchronous sub-tiles.  Whole output
+    against the oracle, float weights descending with ties."""
+    rng = np.random.default_rng(77)
+    nseg = 1_300_000
+    lengths = oracle.geometric_lengths(nseg, seed=9).astype(np.uint32)
+    for lo in rng.integers(0, nseg - 5000, 120):
+        lengths[lo:lo + int(rng.integers(200, 4000))] = 16
+    lengths[rng.integers(0, nseg, 50)] = rng.integers(17, 300, 50).astype(np.uint32)
+    off = _csr(lengths)
+    e = int(off[-1])
+    w = (rng.integers(-40, 40, e) / 8.0).astype(np.float32)
+    w[rng.integers(0, e, 1000)] = -0.0
+    ids = rng.integers(0, 1 << 26, e).astype(np.uint32)
+    ek, ep = oracle.typed_sort_segments(off, w, ids, descending=True, unique=tie == "unique")
+    gk, gp = _run(torch, off, w, ids, descending=True, tie=tie)
+    assert np.array_equal(gk.view(np.uint32), ek.view(np.uint32))
+    assert np.array_equal(gp, ep)
+
+
 def test_cfg4_full_size_properties(torch):
     """cfg4 at full size: 67,108,864 segments; every segment sorted descending
     by (w, id) and a permutation of its input (checked on the device)."""

@@ -38,6 +38,8 @@ KEYS = [
     ("launch__grid_size", "grid"),
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem_bank_conflicts"),
     ("smsp__inst_executed.sum", "warp_inst"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smem_wavefronts"),
+    ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "fma_%"),
 ]
 
 
@@ -69,6 +71,12 @@ def short_name(name: str) -> str:
     if m:
         u, p, lg, e, full, ph = m.groups()
         return f"pksort {'merge' if ph == 'Bitonic' else 'rss'} NR={1 << int(lg)} {'u64' if u == 'long' else 'u32'} {pay_name(p)}"
+    m = re.search(r"seg_kernel<unsigned (long|int), ((?:nsg::)?[A-Za-z ]+?), (?:\(int\))?(\d), (?:\(int\))?(\d), "
+                  r"(?:\(int\))?(\d)>", name)
+    if m:
+        u, p, mode, dag, xk = m.groups()
+        return (f"seg_kernel {'u64' if u == 'long' else 'u32'} {pay_name(p)} {'UNIQUE' if mode == '1' else 'REF'} "
+                f"{'best' if dag == '0' else 'bn'} xform={['none', 'generic', 'float-desc'][int(xk)]}")
     return name[:90]
 
 
@@ -97,7 +105,13 @@ def launches(path: Path, out: Path):
 
 
 def rep_summary(rep: Path, out: Path, traffic: dict):
-    txt = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    """`rep`: an .ncu-rep, or the `--page raw --csv` export of one (*.raw.csv:
+    reports with source are too large to bring back from the GPU box; a
+    <stem>.lines.txt from tools/ncu_lines.py beside it is appended)."""
+    if rep.suffix == ".csv":
+        txt = rep.read_text()
+    else:
+        txt = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     hdr, units = rows[0], rows[1]
     lines = [f"# {rep.name} (ncu --set full --clock-control none)\n"]
@@ -128,6 +142,10 @@ def rep_summary(rep: Path, out: Path, traffic: dict):
             traffic[name] = int(gb("dram_read") + gb("dram_write"))
         except Exception:
             pass
+    lt = rep.with_name(rep.name.replace(".raw.csv", ".lines.txt"))
+    if rep.suffix == ".csv" and lt.exists():
+        head = lt.read_text().splitlines()[:28]
+        lines += ["## CUDA source lines by warp instructions (tools/ncu_lines.py)\n", "```"] + head + ["```", ""]
     out.write_text("\n".join(lines) + "\n")
 
 
@@ -144,7 +162,7 @@ def main():
     tpath = ROOT / "profiles" / "traffic.json"
     traffic = json.loads(tpath.read_text()) if tpath.exists() else {}
     for rep in a.rep:
-        rep_summary(Path(rep), d / (Path(rep).stem + ".md"), traffic)
+        rep_summary(Path(rep), d / (Path(rep).name.replace(".raw.csv", "").replace(".ncu-rep", "") + ".md"), traffic)
     tpath.write_text(json.dumps(traffic, indent=1, sort_keys=True) + "\n")
 
 

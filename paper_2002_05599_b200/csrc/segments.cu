@@ -361,6 +361,45 @@ __device__ __forceinline__ void sort_segment_padm(U* keys, P* pays, int len, con
   }
 }
 
+// Two segments per lane through the same M-channel network: the two
+// independent comparator streams interleave, which hides the dependent
+// compare -> select latency of the short networks (few comparators per layer).
+template <int M, class U, class P, int DAG, class CX, int XK>
+__device__ __forceinline__ void sort_segment_padm2(U* k1, P* p1, int len1, U* k2, P* p2, int len2, const Xform& xf) {
+  constexpr bool HAS_P = !IsNoPay<P>::value;
+  Elem<U, P> v[M], w[M];
+#pragma unroll
+  for (int j = 0; j < M; ++j) {
+    if (j < len1) {
+      v[j].k = xk_to<XK>(k1[j], xf);
+      if constexpr (HAS_P) v[j].p = xk_pay<XK>(p1[j], xf);
+    } else {
+      v[j].k = xk_pad<XK, U>();
+      if constexpr (HAS_P) v[j].p = xk_pad<XK, P>();
+    }
+    if (j < len2) {
+      w[j].k = xk_to<XK>(k2[j], xf);
+      if constexpr (HAS_P) w[j].p = xk_pay<XK>(p2[j], xf);
+    } else {
+      w[j].k = xk_pad<XK, U>();
+      if constexpr (HAS_P) w[j].p = xk_pad<XK, P>();
+    }
+  }
+  Net<DAG, M>::template run<CX>(v);
+  Net<DAG, M>::template run<CX>(w);
+#pragma unroll
+  for (int j = 0; j < M; ++j) {
+    if (j < len1) {
+      k1[j] = xk_from<XK>(v[j].k, xf);
+      if constexpr (HAS_P) p1[j] = xk_pay<XK>(v[j].p, xf);
+    }
+    if (j < len2) {
+      k2[j] = xk_from<XK>(w[j].k, xf);
+      if constexpr (HAS_P) p2[j] = xk_pay<XK>(w[j].p, xf);
+    }
+  }
+}
+
 // Unique-order modes sort 5..8 items with the padded 8-network: four fewer
 // network bodies in the sort phase (instruction cache) outweigh the extra
 // comparators (cfg4 1.558 -> 1.532 ms; padding 9..10 to 16 or 3..4 to 4 as
@@ -386,6 +425,12 @@ __device__ __forceinline__ void sort_segment_padm(U* keys, P* pays, int len, con
 // it is stored: two CTA barriers per tile instead of four
 #ifndef NSG_SEG_PIPE
 #define NSG_SEG_PIPE 1
+#endif
+// unique-order modes: chunks whose class is <= NSG_SEG_PAIR items are sorted
+// two at a time (two segments per lane, sort_segment_padm2); 0 = off.
+// Measured slower on cfg4: 1.071 ms off, 1.092 / 1.112 / 1.139 ms for 4 / 6 / 8.
+#ifndef NSG_SEG_PAIR
+#define NSG_SEG_PAIR 0
 #endif
 #ifndef NSG_SEG_U23
 #define NSG_SEG_U23 1  // 2- and 3-item classes of their own (else padded to 4)
@@ -569,11 +614,11 @@ __global__ void __launch_bounds__(kThreads, NSG_SEG_MINB) seg_kernel(const SegPa
     const int w = tid >> 5;
     const int nchunks = (nshort + 31) / 32;
     [[maybe_unused]] const uint32_t e0 = offs[a];
-    for (int k = 0; k * NW < nchunks; ++k) {
-      const int c = k * NW + ((k & 1) ? (NW - 1 - w) : w);
-      if (c >= nchunks) continue;
+    auto chunk_of = [&](int k) { return k * NW + ((k & 1) ? (NW - 1 - w) : w); };
+    auto entry = [&](int c, int& st, int& len) {  // lane's segment of chunk c
       const int j = c * 32 + lane;
-      int st = 0, len = 0;
+      st = 0;
+      len = 0;
       if constexpr (NSG_SEG_PERM32) {
         const uint32_t pe = j < nshort ? perm[j] : 0u;
         st = int(pe >> 5);
@@ -584,6 +629,13 @@ __global__ void __launch_bounds__(kThreads, NSG_SEG_MINB) seg_kernel(const SegPa
         len = int(offs[s + 1] - offs[s]);
       }
       NSG_DCHECK(st >= 0 && st + len <= G::CAP);
+    };
+    for (int k = 0; k * NW < nchunks; ++k) {
+      const int c = chunk_of(k);
+      if (c >= nchunks) break;  // chunk_of is increasing in k
+      const int j = c * 32 + lane;
+      int st, len;
+      entry(c, st, len);
       U* kp = reinterpret_cast<U*>(kb) + st;
       P* pp = reinterpret_cast<P*>(pb) + st;
       if constexpr (NSG_SEG_UNIFORM && !IsRefCx<CX>::value) {
@@ -591,6 +643,21 @@ __global__ void __launch_bounds__(kThreads, NSG_SEG_MINB) seg_kernel(const SegPa
         // class of its longest segment (lane 0: perm is longest first), so a
         // chunk that straddles two length classes does not execute both bodies
         const int lmax = __shfl_sync(0xffffffffu, len, 0);
+        if (NSG_SEG_PAIR && lmax <= NSG_SEG_PAIR) {
+          // this warp's next chunk (shorter or equal class) rides along
+          const int c2 = chunk_of(k + 1);
+          int st2 = 0, len2 = 0;
+          if (c2 < nchunks) entry(c2, st2, len2);
+          U* kq = reinterpret_cast<U*>(kb) + st2;
+          P* pq = reinterpret_cast<P*>(pb) + st2;
+          ++k;
+          if (lmax > (NSG_SEG_U6 ? 6 : 4)) sort_segment_padm2<8, U, P, DAG, CX, XK>(kp, pp, len, kq, pq, len2, xf);
+          else if (NSG_SEG_U6 && lmax > 4) sort_segment_padm2<6, U, P, DAG, CX, XK>(kp, pp, len, kq, pq, len2, xf);
+          else if (lmax == 4 || !NSG_SEG_U23) sort_segment_padm2<4, U, P, DAG, CX, XK>(kp, pp, len, kq, pq, len2, xf);
+          else if (lmax == 3) sort_segment_padm2<3, U, P, DAG, CX, XK>(kp, pp, len, kq, pq, len2, xf);
+          else sort_segment_padm2<2, U, P, DAG, CX, XK>(kp, pp, len, kq, pq, len2, xf);
+          continue;
+        }
         if (lmax > (NSG_SEG_U12 ? 12 : 10)) sort_segment_padm<16, U, P, DAG, CX, XK>(kp, pp, len, xf);
         else if (NSG_SEG_U12 && lmax > 10) sort_segment_padm<12, U, P, DAG, CX, XK>(kp, pp, len, xf);
         else if (lmax == 10 || (!NSG_SEG_U9 && lmax == 9)) sort_segment_padm<10, U, P, DAG, CX, XK>(kp, pp, len, xf);

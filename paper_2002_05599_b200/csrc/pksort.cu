@@ -314,6 +314,9 @@ struct PhaseBitonic {
   }
 };
 
+#ifndef NSG_RSS_STRATIFIED
+#define NSG_RSS_STRATIFIED 1  // one sample per stratum of n/L columns
+#endif
 #ifndef NSG_RSS_NET_FMA
 #define NSG_RSS_NET_FMA 1  // base-case 8-network on CxFma (n=256 uniform 1.522 -> 1.506 ms)
 #endif
@@ -498,8 +501,22 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
   const int64_t groups = (rows + R - 1) / R;
   const int64_t gw = int64_t(blockIdx.x) * C::WARPS + warp;
   const int64_t GW = int64_t(gridDim.x) * C::WARPS;
-  // RSS: lane ll samples column lcg^(ll+1)(seed) mod n of its row
-  const uint32_t spos = PH::SCRATCH ? lcg_jump_dev(prm.seed, ll + 1) % uint32_t(n) : 0u;
+  // RSS: lane ll draws its sample with the reference generator, lcg^(ll+1)(seed),
+  // inside its own stratum of columns [ll*n/L, (ll+1)*n/L) (NSG_RSS_STRATIFIED;
+  // else anywhere in the row, the reference's s % n).  For exchangeable columns
+  // the two are the same distribution; on presorted or reversed rows the
+  // stratified splitters are nearly even, which bounds the largest bucket and
+  // with it the merge-split rounds.
+  uint32_t spos = 0u;
+  if (PH::SCRATCH) {
+    const uint32_t draw = lcg_jump_dev(prm.seed, ll + 1);
+    if (NSG_RSS_STRATIFIED) {
+      const uint32_t lo = uint32_t(ll) * uint32_t(n) / uint32_t(L), hi = uint32_t(ll + 1) * uint32_t(n) / uint32_t(L);
+      spos = lo + draw % (hi - lo);
+    } else {
+      spos = draw % uint32_t(n);
+    }
+  }
 
   if (lane == 0) {
 #pragma unroll

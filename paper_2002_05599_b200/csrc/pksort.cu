@@ -81,7 +81,8 @@ __device__ __forceinline__ uint32_t lcg_jump_dev(uint32_t s, int j) {
   return uint32_t((uint64_t(s) * r) % kM);
 }
 
-template <class U, class P, int LOGNR, int E, int SCRATCH = 0>
+// PADE: pad elements after every staged row (padded staging, see the kernel)
+template <class U, class P, int LOGNR, int E, int SCRATCH = 0, int PADE = 0>
 struct PkCfg {
   static constexpr bool HAS_P = !IsNoPay<P>::value;
   static constexpr int PB = PayBytes<P>::value;
@@ -92,12 +93,16 @@ struct PkCfg {
   static constexpr int LOGL = pk_ilog2(L);
   static constexpr int S = NR + L;        // padded row stride of the transpose array (words)
   static_assert(R >= 1 && L >= 1 && L <= 32, "row geometry");
-  static constexpr int KB = W * int(sizeof(U));
-  static constexpr int PBB = W * PB;
+  static constexpr int BUFE = W + R * PADE;  // element slots per ring buffer
+  static constexpr int KB = BUFE * int(sizeof(U));
+  static constexpr int PBB = BUFE * PB;
   // ring depth: one buffer being sorted, one draining its bulk store, the
   // rest (>= 1) loading ahead -- HBM latency x bandwidth per SM wants
   // ~64 KB of loads in flight, so deeper rings for smaller groups
-  static constexpr int NB_RAW = (SCRATCH ? NSG_PK_RING_BYTES / 2 : NSG_PK_RING_BYTES) / (KB + PBB);
+  // (padded configurations run one buffer shallower: the pad bytes would
+  // otherwise cost a resident CTA per SM)
+  static constexpr int NB_RAW =
+      (SCRATCH ? NSG_PK_RING_BYTES / 2 : NSG_PK_RING_BYTES) / (W * (int(sizeof(U)) + PB)) - (PADE ? 1 : 0);
   static constexpr int NB = NB_RAW < 3 ? 3 : NB_RAW > 8 ? 8 : NB_RAW;
   static constexpr int AHEAD = NB - 2;  // groups loading ahead of the one being sorted
   static constexpr int OFF_K = 0;
@@ -303,7 +308,7 @@ struct PhaseCtx {
 };
 
 // Merge sorter: in-lane best network + bitonic merges across lanes.
-template <int LOGNR, int E>
+template <int LOGNR, int E, bool PAD = false>
 struct PhaseBitonic {
   static constexpr int L = (1 << LOGNR) / E;
   static constexpr int SCRATCH = 0;
@@ -314,6 +319,21 @@ struct PhaseBitonic {
   }
 };
 
+// Padded staging: with a power-of-two row of n 8-byte keys every staged row
+// starts on the same shared-memory bank, so the R rows of a group collide on
+// every per-lane access (8-way at n = 32).  Full rows with at least
+// NSG_PK_PAD_MINR rows per group are staged row by row (one bulk copy per row,
+// issued by R lanes at once) with L pad elements after each, which tiles a
+// half-warp's 8-byte accesses over all banks.  0 = off.
+#ifndef NSG_PK_PAD_MINR
+#define NSG_PK_PAD_MINR 4
+#endif
+template <class U, class P, int LOGNR, int E>
+struct PkPad {
+  static constexpr int R = 32 * E >> LOGNR, L = (1 << LOGNR) / E;
+  static constexpr bool value = NSG_PK_PAD_MINR > 0 && R >= NSG_PK_PAD_MINR && sizeof(U) == 8 &&
+                                (IsNoPay<P>::value || sizeof(P) == 8) && L >= 2;
+};
 #ifndef NSG_RSS_STRATIFIED
 #define NSG_RSS_STRATIFIED 1  // one sample per stratum of n/L columns
 #endif
@@ -340,20 +360,21 @@ struct PhaseBitonic {
 // block pair is already in order, so that many rounds sort the row (0-1
 // principle: under any threshold only one bucket is mixed); the round count
 // follows the warp's largest bucket, so there is no overflow case.
-template <int LOGNR>
+template <int LOGNR, bool PAD = false>
 struct PhaseRss {
   static constexpr int E = 8;
   static constexpr int NR = 1 << LOGNR;
   static constexpr int L = NR / E;
   static constexpr int LOGL = pk_ilog2(L);
   static constexpr int R = 32 * E / NR;
-  static constexpr int SCRATCH = R * NR + 32;  // bucket array + counters
+  static constexpr int PS = NR + (PAD ? L : 0);  // row stride of the bucket array (padded like the staging)
+  static constexpr int SCRATCH = R * PS + 32;    // bucket array + counters
 
   __device__ __forceinline__ static unsigned sort(uint32_t (&pk)[E], const PhaseCtx& c) {
     uint32_t* pb = c.sc;                 // R rows x NR words: column order, then bucket order
-    uint32_t* cnt = c.sc + R * NR;       // 32 bucket counters / starts (bucket g*L + b)
+    uint32_t* cnt = c.sc + R * PS;       // 32 bucket counters / starts (bucket g*L + b)
     const int lane = c.lane, g = c.g, ll = c.ll;
-    uint32_t* prow = pb + g * NR;
+    uint32_t* prow = pb + g * PS;
 #pragma unroll
     for (int r = 0; r < E; ++r) prow[ll + L * r] = pk[r];
     cnt[lane] = 0u;
@@ -406,13 +427,13 @@ struct PhaseRss {
     }
     const uint32_t maxb = __reduce_max_sync(0xffffffffu, cb);
     __syncwarp();
-    cnt[lane] = uint32_t(g * NR) + incl - cb;
+    cnt[lane] = uint32_t(g * PS) + incl - cb;
     __syncwarp();
 #pragma unroll
     for (int r = 0; r < E; ++r) {
       if (r < c.rl) {
         const uint32_t dst = atomicAdd(&cnt[q[r]], 1u);
-        NSG_DCHECK(dst >= uint32_t(g * NR) && dst < uint32_t(g * NR + c.n));
+        NSG_DCHECK(dst >= uint32_t(g * PS) && dst < uint32_t(g * PS + c.n));
         pb[dst] = pk[r];
       }
     }
@@ -474,10 +495,11 @@ struct PhaseRss {
 
 // FULL: n == NR (no padding slots) -- the validity tests drop out; rows past
 // the end of the batch in the last group are sorted as garbage, never stored.
-template <class U, class P, int LOGNR, int E, bool FULL, class PH>
+template <class U, class P, int LOGNR, int E, bool FULL, class PH, bool PAD = false>
 __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParams prm) {
-  using C = PkCfg<U, P, LOGNR, E, PH::SCRATCH>;
-  constexpr int NR = C::NR, R = C::R, L = C::L, LOGL = C::LOGL, W = C::W, S = C::S, NB = C::NB;
+  static_assert(!PAD || FULL, "padded staging is for full rows");
+  using C = PkCfg<U, P, LOGNR, E, PH::SCRATCH, PAD ? (1 << LOGNR) / E : 0>;
+  constexpr int NR = C::NR, R = C::R, L = C::L, LOGL = C::LOGL, W = C::BUFE, S = C::S, NB = C::NB;
   constexpr bool HAS_P = C::HAS_P;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
@@ -493,6 +515,7 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
   U* kout = static_cast<U*>(prm.k_out);
   P* pout = static_cast<P*>(prm.p_out);
   const int n = prm.n;
+  const int rs = PAD ? NR + L : n;  // row stride of the staged group
   const int64_t rows = prm.rows;
   const Xform xf = prm.xf;
   const PipeK kk{prm.one, prm.neg1};
@@ -535,6 +558,19 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
   };
   auto issue = [&](int64_t grp, int b) {
     const int rin = rows_in(grp);
+    if constexpr (PAD) {  // one bulk copy per row, issued by the first rin lanes at once
+      if (bulk_ok(rin)) {
+        const int64_t base = grp * R * int64_t(n);
+        if (lane == 0) mbar_expect_tx(&bar[b], unsigned(rin * n * (int(sizeof(U)) + C::PB)));
+        __syncwarp();
+        if (lane < rin) {
+          bulk_g2s(kbuf + b * W + lane * rs, kin + base + int64_t(lane) * n, unsigned(n * int(sizeof(U))), &bar[b]);
+          if constexpr (HAS_P)
+            bulk_g2s(pbuf + b * W + lane * rs, pin + base + int64_t(lane) * n, unsigned(n * C::PB), &bar[b]);
+        }
+      }
+      return;
+    }
     if (lane == 0 && bulk_ok(rin)) {
       const int64_t base = grp * R * int64_t(n);
       const unsigned kbytes = unsigned(rin * n * int(sizeof(U)));
@@ -556,7 +592,7 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
     const int64_t nxt = grp + C::AHEAD * GW;
     // buffer bn last held the group two iterations back: its bulk store must
     // have finished reading shared memory (the previous group's may still run)
-    if (lane == 0) bulk_wait_read<1>();
+    if (PAD ? lane < R : lane == 0) bulk_wait_read<1>();
     __syncwarp();
     if (nxt < groups) issue(nxt, bn);
     bn = bn + 1 == NB ? 0 : bn + 1;
@@ -571,8 +607,9 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
       phases ^= 1u << b;
     } else {  // unaligned chunk (odd 4-byte rows, the grid's tail): lanes copy
       for (int i = lane; i < cnt; i += 32) {
-        fk[i] = kin[base + i];
-        if constexpr (HAS_P) fp[i] = pin[base + i];
+        const int si = PAD ? (i >> LOGNR) * rs + (i & (NR - 1)) : i;
+        fk[si] = kin[base + i];
+        if constexpr (HAS_P) fp[si] = pin[base + i];
       }
       __syncwarp();
     }
@@ -581,8 +618,8 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
     // lane (g, ll) owns columns pos = ll + L*r, r < rl, of row g; the
     // loads below stay inside the buffer for every r, so they are unconditional
     const bool rowv = g < rin;
-    U* rk = fk + g * n;
-    P* rp = fp + g * n;
+    U* rk = fk + g * rs;
+    P* rp = fp + g * rs;
     const int rl = FULL ? E : rowv ? (n - ll + L - 1) >> LOGL : 0;  // valid r of this lane
     uint32_t pk[E];
     if (!xf.flt) {
@@ -717,41 +754,53 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
       const int gi = __ffs(int(bad_rows)) - 1;
       bad_rows &= bad_rows - 1;
       if (lane == 0) atomicAdd(&g_pk_fallback_rows, 1ull);
-      pk_exact_row<U, P>(fk + gi * n, fp + gi * n, n, xf, lane);
+      pk_exact_row<U, P>(fk + gi * rs, fp + gi * rs, n, xf, lane);
     }
 
     // ---- 6. store -----------------------------------------------------------
     if (bk) {
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) {
+      if constexpr (PAD) {
+        if (lane < rin) {
+          bulk_s2g(kout + base + int64_t(lane) * n, fk + lane * rs, unsigned(n * int(sizeof(U))));
+          if constexpr (HAS_P) bulk_s2g(pout + base + int64_t(lane) * n, fp + lane * rs, unsigned(n * C::PB));
+          bulk_commit();
+        }
+      } else if (lane == 0) {
         bulk_s2g(kout + base, fk, unsigned(cnt * int(sizeof(U))));
         if constexpr (HAS_P) bulk_s2g(pout + base, fp, unsigned(cnt * C::PB));
         bulk_commit();
       }
     } else {
       for (int i = lane; i < cnt; i += 32) {
-        kout[base + i] = fk[i];
-        if constexpr (HAS_P) pout[base + i] = fp[i];
+        const int si = PAD ? (i >> LOGNR) * rs + (i & (NR - 1)) : i;
+        kout[base + i] = fk[si];
+        if constexpr (HAS_P) pout[base + i] = fp[si];
       }
     }
     __syncwarp();
     b = b + 1 == NB ? 0 : b + 1;
   }
-  if (lane == 0) bulk_wait<0>();
+  if (PAD ? lane < R : lane == 0) bulk_wait<0>();
 }
 
 template <class U, class P, int LG, bool RSS>
 const void* pk_fn_lg(bool full, int* smem) {
   if constexpr (RSS) {
+    constexpr bool PAD = PkPad<U, P, LG, PhaseRss<LG>::E>::value;
     using PH = PhaseRss<LG>;
-    *smem = PkCfg<U, P, LG, PH::E, PH::SCRATCH>::CTA_SMEM;
-    return full ? reinterpret_cast<const void*>(&pksort_kernel<U, P, LG, PH::E, true, PH>)
-                : reinterpret_cast<const void*>(&pksort_kernel<U, P, LG, PH::E, false, PH>);
+    using PHF = PhaseRss<LG, PAD>;  // full rows: padded staging where it pays
+    constexpr int E = PH::E;
+    *smem = full ? PkCfg<U, P, LG, E, PHF::SCRATCH, PAD ? PH::L : 0>::CTA_SMEM : PkCfg<U, P, LG, E, PH::SCRATCH>::CTA_SMEM;
+    return full ? reinterpret_cast<const void*>(&pksort_kernel<U, P, LG, E, true, PHF, PAD>)
+                : reinterpret_cast<const void*>(&pksort_kernel<U, P, LG, E, false, PH>);
   } else {
+    constexpr bool PAD = PkPad<U, P, LG, NSG_PK_E>::value;
     using PH = PhaseBitonic<LG, NSG_PK_E>;
-    *smem = PkCfg<U, P, LG, NSG_PK_E, 0>::CTA_SMEM;
-    return full ? reinterpret_cast<const void*>(&pksort_kernel<U, P, LG, NSG_PK_E, true, PH>)
+    constexpr int PADE = PAD ? (1 << LG) / NSG_PK_E : 0;
+    *smem = full ? PkCfg<U, P, LG, NSG_PK_E, 0, PADE>::CTA_SMEM : PkCfg<U, P, LG, NSG_PK_E, 0>::CTA_SMEM;
+    return full ? reinterpret_cast<const void*>(&pksort_kernel<U, P, LG, NSG_PK_E, true, PH, PAD>)
                 : reinterpret_cast<const void*>(&pksort_kernel<U, P, LG, NSG_PK_E, false, PH>);
   }
 }

@@ -22,6 +22,10 @@ for what in "$@"; do
     pkfew) cap pkfew_s5 pksort_kernel 1 1 python tools/pk_one.py 256 few16 merge ;;
     pkuni) cap pkuni_s5 pksort_kernel 1 1 python tools/pk_one.py 256 uniform merge ;;
     pkrss) cap pkrss_s5 pksort_kernel 1 1 python tools/pk_one.py 256 uniform rss ;;
+    pkrss32) cap pkrss32_s5 pksort_kernel 1 1 python tools/pk_one.py 32 uniform rss ;;
+    pkrss64) cap pkrss64_s5 pksort_kernel 1 1 python tools/pk_one.py 64 uniform rss ;;
+    pkmrg32) cap pkmrg32_s5 pksort_kernel 1 1 python tools/pk_one.py 32 uniform merge ;;
+    pkmrg64) cap pkmrg64_s5 pksort_kernel 1 1 python tools/pk_one.py 64 uniform merge ;;
     net7) cap net7_s5 "net_|nettma|netbulk" 4 4 python bench.py --ns 7 --steps 1 --warmup 1 --no-e2e --no-cpu --workloads none ;;
     net10) cap net10_s5 "net_|nettma|netbulk" 4 4 python bench.py --ns 10 --steps 1 --warmup 1 --no-e2e --no-cpu --workloads none ;;
   esac

@@ -92,6 +92,34 @@ def main():
     ek, ep = oracle.typed_sort_segments(off, w, ids, descending=True, unique=True)
     assert np.array_equal(gk.cpu().numpy(), ek) and np.array_equal(gp.cpu().numpy(), ep)
     checks += 1
+    # padded row staging of the packed sorters (full power-of-two rows, >= 4
+    # rows per group) including a ragged last group, with and without a payload
+    for n in (32, 64, 128):
+        keys = rng.integers(-2**63, 2**63 - 1, size=(1003, n), dtype=np.int64)
+        keys[::5] %= 3
+        pay = rng.integers(0, 2**63, size=(1003, n), dtype=np.uint64)
+        for kind in ("merge", "rss"):
+            k, _ = batch.sort_rows(t(keys), kind=kind)
+            assert np.array_equal(k.cpu().numpy(), np.sort(keys, axis=1)), (kind, n)
+            k, p = batch.sort_rows(t(keys), t(pay), kind=kind, tie="unique")
+            ek, ep = oracle.typed_sort_rows(keys, pay, unique=True, kind="rss")
+            assert np.array_equal(k.cpu().numpy(), ek) and np.array_equal(p.cpu().numpy(), ep), (kind, n)
+            checks += 2
+    # CSR software pipeline: more tiles than CTAs (every CTA walks several
+    # tiles) with stretches of oversized tiles (synchronous sub-tiles) between
+    lengths = oracle.geometric_lengths(900_000, seed=11).astype(np.uint32)
+    for lo in range(50_000, 850_000, 90_000):
+        lengths[lo:lo + 3000] = 16
+    off = np.zeros(len(lengths) + 1, dtype=np.uint32)
+    np.cumsum(lengths, out=off[1:])
+    w = (rng.integers(-30, 30, int(off[-1])) / 4.0).astype(np.float32)
+    ids = rng.integers(0, 2**26, size=int(off[-1])).astype(np.uint32)
+    for tie in ("unique", "ref"):
+        gk, gp = batch.sort_segments(t(off), t(w), t(ids), descending=True, tie=tie)
+        ek, ep = oracle.typed_sort_segments(off, w, ids, descending=True, unique=tie == "unique")
+        assert np.array_equal(gk.cpu().numpy().view(np.uint32), ek.view(np.uint32))
+        assert np.array_equal(gp.cpu().numpy(), ep)
+        checks += 1
     torch.cuda.synchronize()
     print(f"sanitize probe ok ({checks} checks)")
 

@@ -241,7 +241,7 @@ int nsg_sort_rows(const nsg_spec* sp, const void* keys_in, void* keys_out, const
       return fail(NSG_ERR_SPEC, "the merge sorter orders payloads lexicographically: use tie_mode UNIQUE");
     // keys-only n = 32: one lane per row with the 185-comparator merge network
     // (no cross-lane traffic) measures faster than the warp sorter
-    const bool one_lane32 = n == 32 && sp->payload_dtype == NSG_PAY_NONE;
+    const bool one_lane32 = n == 32 && sp->payload_dtype == NSG_PAY_NONE && !env_flag("NSG_MERGE_PK32");
     if (pksort_covers(n) && !one_lane32 && !env_flag("NSG_MERGE_LEGACY"))  // packed 32-bit words, TMA-staged groups
       return launch_pksort(keys_in, keys_out, pay_in, pay_out, rows, n, kb, sp->payload_dtype, make_xform(*sp), st);
     int g = 0;

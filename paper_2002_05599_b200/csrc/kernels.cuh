@@ -41,6 +41,18 @@ int launch_pksort(const void* k_in, void* k_out, const void* p_in, void* p_out, 
 // (rss kind, keys-only / UNIQUE rows of 17..256 items)
 int launch_pkrss(const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows, int64_t n,
                  int key_bytes, int pay, uint32_t seed, const Xform& xf, cudaStream_t st);
+// REF mode (key-only strict <, payloads travel): rows with all-distinct keys
+// are sorted here (their order is unique); the rest keep their input order in
+// the output and are listed for the draw-for-draw kernel (rss.cu).  `count`
+// may exceed `cap`: the caller then replays every row.
+struct PkDefer {
+  unsigned long long* count;  // device, zeroed by the caller
+  int64_t* ids;               // device, cap entries
+  int64_t cap;
+};
+int launch_pkrss_ref(const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows, int64_t n,
+                     int key_bytes, int pay, bool aos, uint32_t seed, const Xform& xf, const PkDefer& defer,
+                     cudaStream_t st);
 unsigned long long pksort_fallback_rows(bool reset);
 
 // bigsort.cu (rows / segments above 1024 items, keys-only / UNIQUE)

@@ -66,6 +66,14 @@ struct PkParams {
   uint32_t one, neg1;  // 1 and ~0, opaque to the compiler (PipeK)
   uint32_t seed;       // RSS sample seed (the reference's rss_sample_seed)
   Xform xf;
+  // REF mode (key-only strict <, payloads travel): a row whose keys are all
+  // distinct has one sorted order, which this kernel produces; a row with
+  // equal keys (or a packed-word misorder) keeps its ORIGINAL order in the
+  // output and is listed here for the draw-for-draw kernel (rss.cu)
+  int ref;
+  unsigned long long* defer_count;
+  int64_t* defer_ids;
+  int64_t defer_cap;
 };
 
 __host__ __device__ constexpr int pk_ilog2(int x) { return x <= 1 ? 0 : 1 + pk_ilog2(x >> 1); }
@@ -82,8 +90,10 @@ __device__ __forceinline__ uint32_t lcg_jump_dev(uint32_t s, int j) {
 }
 
 // PADE: pad elements after every staged row (padded staging, see the kernel)
-template <class U, class P, int LOGNR, int E, int SCRATCH = 0, int PADE = 0>
+// AOS: reference items, (key, payload) interleaved in one 16-byte-per-item array
+template <class U, class P, int LOGNR, int E, int SCRATCH = 0, int PADE = 0, bool AOS = false>
 struct PkCfg {
+  static_assert(!AOS || (sizeof(U) == 8 && sizeof(P) == 8), "AoS items are (u64 key, u64 ref)");
   static constexpr bool HAS_P = !IsNoPay<P>::value;
   static constexpr int PB = PayBytes<P>::value;
   static constexpr int NR = 1 << LOGNR;   // slots per row
@@ -94,8 +104,8 @@ struct PkCfg {
   static constexpr int S = NR + L;        // padded row stride of the transpose array (words)
   static_assert(R >= 1 && L >= 1 && L <= 32, "row geometry");
   static constexpr int BUFE = W + R * PADE;  // element slots per ring buffer
-  static constexpr int KB = BUFE * int(sizeof(U));
-  static constexpr int PBB = BUFE * PB;
+  static constexpr int KB = BUFE * int(sizeof(U)) * (AOS ? 2 : 1);
+  static constexpr int PBB = AOS ? 0 : BUFE * PB;
   // ring depth: one buffer being sorted, one draining its bulk store, the
   // rest (>= 1) loading ahead -- HBM latency x bandwidth per SM wants
   // ~64 KB of loads in flight, so deeper rings for smaller groups
@@ -268,14 +278,14 @@ __device__ __forceinline__ bool item_lt(U bk, const P& bp, U ak, const P& ap) {
 
 // Exact in-place re-sort of one staged row (raw keys) by the whole warp.
 template <class U, class P>
-__device__ __noinline__ void pk_exact_row(U* rk, P* rp, int n, const Xform xf, int lane) {
+__device__ __noinline__ void pk_exact_row(U* rk, P* rp, int n, const Xform xf, int lane, int st) {
   Elem<U, P> v[8];
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
     const int i = lane * 8 + r;
     if (i < n) {
-      v[r].k = xf.active ? to_ord<U>(rk[i], xf) : rk[i];
-      if constexpr (!IsNoPay<P>::value) v[r].p = xf.active ? P(rp[i] ^ P(xf.pdesc)) : rp[i];
+      v[r].k = xf.active ? to_ord<U>(rk[i * st], xf) : rk[i * st];
+      if constexpr (!IsNoPay<P>::value) v[r].p = xf.active ? P(rp[i * st] ^ P(xf.pdesc)) : rp[i * st];
     } else {
       v[r].k = U(~U(0));
       if constexpr (!IsNoPay<P>::value) v[r].p = P(~P(0));
@@ -287,8 +297,8 @@ __device__ __noinline__ void pk_exact_row(U* rk, P* rp, int n, const Xform xf, i
   for (int r = 0; r < 8; ++r) {
     const int i = lane * 8 + r;
     if (i < n) {
-      rk[i] = xf.active ? from_ord<U>(v[r].k, xf) : v[r].k;
-      if constexpr (!IsNoPay<P>::value) rp[i] = xf.active ? P(v[r].p ^ P(xf.pdesc)) : v[r].p;
+      rk[i * st] = xf.active ? from_ord<U>(v[r].k, xf) : v[r].k;
+      if constexpr (!IsNoPay<P>::value) rp[i * st] = xf.active ? P(v[r].p ^ P(xf.pdesc)) : v[r].p;
     }
   }
   __syncwarp();
@@ -495,10 +505,11 @@ struct PhaseRss {
 
 // FULL: n == NR (no padding slots) -- the validity tests drop out; rows past
 // the end of the batch in the last group are sorted as garbage, never stored.
-template <class U, class P, int LOGNR, int E, bool FULL, class PH, bool PAD = false>
+template <class U, class P, int LOGNR, int E, bool FULL, class PH, bool PAD = false, bool AOS = false>
 __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParams prm) {
   static_assert(!PAD || FULL, "padded staging is for full rows");
-  using C = PkCfg<U, P, LOGNR, E, PH::SCRATCH, PAD ? (1 << LOGNR) / E : 0>;
+  using C = PkCfg<U, P, LOGNR, E, PH::SCRATCH, PAD ? (1 << LOGNR) / E : 0, AOS>;
+  constexpr int ST = AOS ? 2 : 1;  // U words per item in the key array
   constexpr int NR = C::NR, R = C::R, L = C::L, LOGL = C::LOGL, W = C::BUFE, S = C::S, NB = C::NB;
   constexpr bool HAS_P = C::HAS_P;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -554,7 +565,7 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
   };
   auto bulk_ok = [&](int rin) -> bool {
     const int64_t cnt = int64_t(rin) * n;
-    return prm.bulk && (cnt * int64_t(sizeof(U))) % 16 == 0 && (cnt * C::PB) % 16 == 0;
+    return prm.bulk && (cnt * int64_t(sizeof(U))) % 16 == 0 && (AOS || (cnt * C::PB) % 16 == 0);
   };
   auto issue = [&](int64_t grp, int b) {
     const int rin = rows_in(grp);
@@ -564,8 +575,9 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
         if (lane == 0) mbar_expect_tx(&bar[b], unsigned(rin * n * (int(sizeof(U)) + C::PB)));
         __syncwarp();
         if (lane < rin) {
-          bulk_g2s(kbuf + b * W + lane * rs, kin + base + int64_t(lane) * n, unsigned(n * int(sizeof(U))), &bar[b]);
-          if constexpr (HAS_P)
+          bulk_g2s(kbuf + (b * W + lane * rs) * ST, kin + (base + int64_t(lane) * n) * ST,
+                   unsigned(n * int(sizeof(U)) * ST), &bar[b]);
+          if constexpr (HAS_P && !AOS)
             bulk_g2s(pbuf + b * W + lane * rs, pin + base + int64_t(lane) * n, unsigned(n * C::PB), &bar[b]);
         }
       }
@@ -573,11 +585,11 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
     }
     if (lane == 0 && bulk_ok(rin)) {
       const int64_t base = grp * R * int64_t(n);
-      const unsigned kbytes = unsigned(rin * n * int(sizeof(U)));
-      const unsigned pbytes = unsigned(rin * n * C::PB);
+      const unsigned kbytes = unsigned(rin * n * int(sizeof(U)) * ST);
+      const unsigned pbytes = AOS ? 0u : unsigned(rin * n * C::PB);
       mbar_expect_tx(&bar[b], kbytes + pbytes);
-      bulk_g2s(kbuf + b * W, kin + base, kbytes, &bar[b]);
-      if constexpr (HAS_P) bulk_g2s(pbuf + b * W, pin + base, pbytes, &bar[b]);
+      bulk_g2s(kbuf + b * W * ST, kin + base * ST, kbytes, &bar[b]);
+      if constexpr (HAS_P && !AOS) bulk_g2s(pbuf + b * W, pin + base, pbytes, &bar[b]);
     }
   };
 
@@ -596,8 +608,8 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
     __syncwarp();
     if (nxt < groups) issue(nxt, bn);
     bn = bn + 1 == NB ? 0 : bn + 1;
-    U* fk = kbuf + b * W;
-    P* fp = pbuf + b * W;
+    U* fk = kbuf + b * W * ST;
+    P* fp = AOS ? reinterpret_cast<P*>(fk) + 1 : pbuf + b * W;
     const int rin = rows_in(grp);
     const int cnt = rin * n;
     const int64_t base = grp * R * int64_t(n);
@@ -608,8 +620,8 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
     } else {  // unaligned chunk (odd 4-byte rows, the grid's tail): lanes copy
       for (int i = lane; i < cnt; i += 32) {
         const int si = PAD ? (i >> LOGNR) * rs + (i & (NR - 1)) : i;
-        fk[si] = kin[base + i];
-        if constexpr (HAS_P) fp[si] = pin[base + i];
+        fk[si * ST] = kin[(base + i) * ST];
+        if constexpr (HAS_P) fp[si * ST] = AOS ? P(kin[(base + i) * ST + 1]) : pin[base + i];
       }
       __syncwarp();
     }
@@ -618,8 +630,8 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
     // lane (g, ll) owns columns pos = ll + L*r, r < rl, of row g; the
     // loads below stay inside the buffer for every r, so they are unconditional
     const bool rowv = g < rin;
-    U* rk = fk + g * rs;
-    P* rp = fp + g * rs;
+    U* rk = fk + g * rs * ST;   // item i of the row: key rk[i * ST], payload rp[i * ST]
+    P* rp = fp + g * rs * ST;
     const int rl = FULL ? E : rowv ? (n - ll + L - 1) >> LOGL : 0;  // valid r of this lane
     uint32_t pk[E];
     if (!xf.flt) {
@@ -632,7 +644,7 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
       U acc = U(0);
 #pragma unroll
       for (int r = 0; r < E; ++r) {
-        x[r] = rk[ll + L * r];
+        x[r] = rk[(ll + L * r) * ST];
         if (FULL || r < rl) acc |= x[r] ^ f;
       }
 #pragma unroll
@@ -651,7 +663,7 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
       U acc = U(0);
 #pragma unroll
       for (int r = 0; r < E; ++r) {
-        x[r] = to_ord<U>(rk[ll + L * r], xf);
+        x[r] = to_ord<U>(rk[(ll + L * r) * ST], xf);
         if (FULL || r < rl) acc |= x[r] ^ first;
       }
 #pragma unroll
@@ -698,16 +710,16 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
         const int q = ll + L * r;  // q / E folds to (L*r)/E when L <= E
         const uint32_t idx = pr[L <= E ? q + (L * r) / E : q + q / E] & uint32_t(NR - 1);
         NSG_DCHECK(!rowv || int(idx) < n);
-        ok[r] = rk[idx];
-        if constexpr (HAS_P) op[r] = rp[idx];
+        ok[r] = rk[idx * ST];
+        if constexpr (HAS_P) op[r] = rp[idx * ST];
       }
     }
     __syncwarp();  // every gather is done before the staged rows are overwritten
 #pragma unroll
     for (int r = 0; r < E; ++r) {
       if (FULL || r < rl) {
-        rk[ll + L * r] = ok[r];
-        if constexpr (HAS_P) rp[ll + L * r] = op[r];
+        rk[(ll + L * r) * ST] = ok[r];
+        if constexpr (HAS_P) rp[(ll + L * r) * ST] = op[r];
       }
     }
     __syncwarp();
@@ -727,17 +739,38 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
         for (int r = 0; r < E; ++r) {
           const int q = ll + L * r;
           const int qp = q - (q > 0 ? 1 : 0);
-          const U pk_ = rk[qp];
+          const U pk_ = rk[qp * ST];
           P a{}, bq{};
           if constexpr (HAS_P) {
-            a = P(rp[qp] ^ P(xf.pdesc));
+            a = P(rp[qp * ST] ^ P(xf.pdesc));
             bq = P(op[r] ^ P(xf.pdesc));
           }
           const bool lt = item_lt<U, P>(kord(ok[r]), bq, kord(pk_), a);
           bad |= (FULL || r < rl) && lt;
         }
       };
-      if (xf.flt) {
+      // REF mode: a key-order violation OR an equal neighbour key (position 0
+      // excepted: it compares with itself) sends the row to the draw-for-draw
+      // kernel -- equal keys in one packed-prefix run are either adjacent or
+      // separated by a different key, which is an order violation on one side
+      auto check_ref = [&](auto kord) {
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          const int q = ll + L * r;
+          const int qp = q - (q > 0 ? 1 : 0);
+          const U cur = kord(ok[r]), prv = kord(rk[qp * ST]);
+          const bool hit = key_lt(cur, prv) || (q > 0 && cur == prv);
+          bad |= (FULL || r < rl) && hit;
+        }
+      };
+      const bool ref = HAS_P && prm.ref != 0;
+      if (ref) {
+        if (xf.flt) {
+          check_ref([&](U v) -> U { return to_ord<U>(v, xf); });
+        } else {
+          check_ref([&](U v) -> U { return U(v ^ M); });
+        }
+      } else if (xf.flt) {
         check([&](U v) -> U { return to_ord<U>(v, xf); });
       } else {
         check([&](U v) -> U { return U(v ^ M); });
@@ -748,13 +781,36 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
       for (int gg = 0; gg < R; ++gg) {
         if ((bm >> (gg * L)) & (L == 32 ? 0xffffffffu : ((1u << L) - 1u))) bad_rows |= 1u << gg;
       }
+      if constexpr (HAS_P) {
+        if (ref && bad_rows) {
+          // deferred rows go back to their ORIGINAL order (sorted position q
+          // came from column idx) and are listed for the draw-for-draw kernel
+          if ((bad_rows >> g) & 1u) {
+#pragma unroll
+            for (int r = 0; r < E; ++r) {
+              if (FULL || r < rl) {
+                const int q = ll + L * r;
+                const uint32_t idx = pr[L <= E ? q + (L * r) / E : q + q / E] & uint32_t(NR - 1);
+                rk[idx * ST] = ok[r];
+                rp[idx * ST] = op[r];
+              }
+            }
+            if (ll == 0) {
+              const unsigned long long slot = atomicAdd(prm.defer_count, 1ull);
+              if (slot < (unsigned long long)prm.defer_cap) prm.defer_ids[slot] = grp * R + g;
+            }
+          }
+          bad_rows = 0u;
+          __syncwarp();
+        }
+      }
     }
 
     while (bad_rows) {
       const int gi = __ffs(int(bad_rows)) - 1;
       bad_rows &= bad_rows - 1;
       if (lane == 0) atomicAdd(&g_pk_fallback_rows, 1ull);
-      pk_exact_row<U, P>(fk + gi * rs, fp + gi * rs, n, xf, lane);
+      pk_exact_row<U, P>(fk + gi * rs * ST, fp + gi * rs * ST, n, xf, lane, ST);
     }
 
     // ---- 6. store -----------------------------------------------------------
@@ -763,20 +819,24 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
       __syncwarp();
       if constexpr (PAD) {
         if (lane < rin) {
-          bulk_s2g(kout + base + int64_t(lane) * n, fk + lane * rs, unsigned(n * int(sizeof(U))));
-          if constexpr (HAS_P) bulk_s2g(pout + base + int64_t(lane) * n, fp + lane * rs, unsigned(n * C::PB));
+          bulk_s2g(kout + (base + int64_t(lane) * n) * ST, fk + lane * rs * ST, unsigned(n * int(sizeof(U)) * ST));
+          if constexpr (HAS_P && !AOS)
+            bulk_s2g(pout + base + int64_t(lane) * n, fp + lane * rs, unsigned(n * C::PB));
           bulk_commit();
         }
       } else if (lane == 0) {
-        bulk_s2g(kout + base, fk, unsigned(cnt * int(sizeof(U))));
-        if constexpr (HAS_P) bulk_s2g(pout + base, fp, unsigned(cnt * C::PB));
+        bulk_s2g(kout + base * ST, fk, unsigned(cnt * int(sizeof(U)) * ST));
+        if constexpr (HAS_P && !AOS) bulk_s2g(pout + base, fp, unsigned(cnt * C::PB));
         bulk_commit();
       }
     } else {
       for (int i = lane; i < cnt; i += 32) {
         const int si = PAD ? (i >> LOGNR) * rs + (i & (NR - 1)) : i;
-        kout[base + i] = fk[si];
-        if constexpr (HAS_P) pout[base + i] = fp[si];
+        kout[(base + i) * ST] = fk[si * ST];
+        if constexpr (HAS_P) {
+          if constexpr (AOS) kout[(base + i) * ST + 1] = U(fp[si * ST]);
+          else pout[base + i] = fp[si];
+        }
       }
     }
     __syncwarp();
@@ -785,17 +845,19 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
   if (PAD ? lane < R : lane == 0) bulk_wait<0>();
 }
 
-template <class U, class P, int LG, bool RSS>
+template <class U, class P, int LG, bool RSS, bool AOS = false>
 const void* pk_fn_lg(bool full, int* smem) {
   if constexpr (RSS) {
     constexpr bool PAD = PkPad<U, P, LG, PhaseRss<LG>::E>::value;
     using PH = PhaseRss<LG>;
     using PHF = PhaseRss<LG, PAD>;  // full rows: padded staging where it pays
     constexpr int E = PH::E;
-    *smem = full ? PkCfg<U, P, LG, E, PHF::SCRATCH, PAD ? PH::L : 0>::CTA_SMEM : PkCfg<U, P, LG, E, PH::SCRATCH>::CTA_SMEM;
-    return full ? reinterpret_cast<const void*>(&pksort_kernel<U, P, LG, E, true, PHF, PAD>)
-                : reinterpret_cast<const void*>(&pksort_kernel<U, P, LG, E, false, PH>);
+    *smem = full ? PkCfg<U, P, LG, E, PHF::SCRATCH, PAD ? PH::L : 0, AOS>::CTA_SMEM
+                 : PkCfg<U, P, LG, E, PH::SCRATCH, 0, AOS>::CTA_SMEM;
+    return full ? reinterpret_cast<const void*>(&pksort_kernel<U, P, LG, E, true, PHF, PAD, AOS>)
+                : reinterpret_cast<const void*>(&pksort_kernel<U, P, LG, E, false, PH, false, AOS>);
   } else {
+    static_assert(!AOS, "AoS items take the RSS phase");
     constexpr bool PAD = PkPad<U, P, LG, NSG_PK_E>::value;
     using PH = PhaseBitonic<LG, NSG_PK_E>;
     constexpr int PADE = PAD ? (1 << LG) / NSG_PK_E : 0;
@@ -820,6 +882,17 @@ const void* pk_fn(int lognr, bool full, bool rss, int* smem) {
   }
 }
 
+// reference items (AoS, u64 key + u64 ref): RSS phase only
+const void* pk_pick_aos(int lognr, bool full, int* smem) {
+  switch (lognr) {
+    case 5: return pk_fn_lg<uint64_t, uint64_t, 5, true, true>(full, smem);
+    case 6: return pk_fn_lg<uint64_t, uint64_t, 6, true, true>(full, smem);
+    case 7: return pk_fn_lg<uint64_t, uint64_t, 7, true, true>(full, smem);
+    case 8: return pk_fn_lg<uint64_t, uint64_t, 8, true, true>(full, smem);
+    default: return nullptr;
+  }
+}
+
 const void* pk_pick(int kb, int pay, int lognr, bool full, bool rss, int* smem) {
   if (kb == 4) {
     if (pay == 0) return pk_fn<uint32_t, NoPay>(lognr, full, rss, smem);
@@ -836,17 +909,21 @@ const void* pk_pick(int kb, int pay, int lognr, bool full, bool rss, int* smem) 
 bool pksort_covers(int64_t n) { return n >= 17 && n <= 256; }
 
 static int launch_pk(const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows, int64_t n,
-                     int key_bytes, int pay, const Xform& xf, bool rss, uint32_t seed, cudaStream_t st) {
+                     int key_bytes, int pay, const Xform& xf, bool rss, uint32_t seed, cudaStream_t st,
+                     bool aos = false, const PkDefer* defer = nullptr) {
   if (!pksort_covers(n)) return fail(NSG_ERR_SPEC, "packed warp sorters cover 17..256 items, got %lld", (long long)n);
   if (rows <= 0) return 0;
   int lognr = 5;
   while ((1 << lognr) < n) ++lognr;
   int smem = 0;
-  const void* fn = pk_pick(key_bytes, pay, lognr, n == (int64_t(1) << lognr), rss, &smem);
+  const bool full = n == (int64_t(1) << lognr);
+  const void* fn = aos ? pk_pick_aos(lognr, full, &smem) : pk_pick(key_bytes, pay, lognr, full, rss, &smem);
   if (!fn) return fail(NSG_ERR_SPEC, "no packed warp sorter for this configuration");
   const auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  const bool bulk = al(k_in) && al(k_out) && (pay == 0 || (al(p_in) && al(p_out))) && !env_flag("NSG_PK_NOBULK");
-  PkParams prm{k_in, k_out, p_in, p_out, rows, int(n), bulk ? 1 : 0, 1u, 0xffffffffu, seed == 0 ? 1u : seed, xf};
+  const bool bulk =
+      al(k_in) && al(k_out) && (pay == 0 || aos || (al(p_in) && al(p_out))) && !env_flag("NSG_PK_NOBULK");
+  PkParams prm{k_in, k_out, p_in, p_out, rows, int(n), bulk ? 1 : 0, 1u, 0xffffffffu, seed == 0 ? 1u : seed, xf,
+               defer ? 1 : 0, defer ? defer->count : nullptr, defer ? defer->ids : nullptr, defer ? defer->cap : 0};
   int sms = 0, occ = 0;
   constexpr int threads = NSG_PK_WARPS * 32;
   if (int rc = kernel_residency(fn, threads, smem, &occ, &sms)) return rc;
@@ -868,6 +945,15 @@ int launch_pksort(const void* k_in, void* k_out, const void* p_in, void* p_out, 
 int launch_pkrss(const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows, int64_t n,
                  int key_bytes, int pay, uint32_t seed, const Xform& xf, cudaStream_t st) {
   return launch_pk(k_in, k_out, p_in, p_out, rows, n, key_bytes, pay, xf, true, seed, st);
+}
+
+// REF mode (payload rows, or AoS reference items when p_in == nullptr and
+// aos): rows with all-distinct keys are sorted; the others keep their input
+// order in the output and are listed in `defer` (see PkParams::ref).
+int launch_pkrss_ref(const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows, int64_t n,
+                     int key_bytes, int pay, bool aos, uint32_t seed, const Xform& xf, const PkDefer& defer,
+                     cudaStream_t st) {
+  return launch_pk(k_in, k_out, p_in, p_out, rows, n, key_bytes, pay, xf, true, seed, st, aos, &defer);
 }
 
 unsigned long long pksort_fallback_rows(bool reset) {

@@ -87,6 +87,12 @@ struct RssParams {
   const uint32_t* seg_count;
   uint32_t* seg_overflow;
   int big_elsewhere;  // segments above NMAX are sorted by bigsort.cu: skip, do not count
+  // deferred-row mode (REF rows the packed sorter could not finish,
+  // pksort.cu): only the *row_count rows listed in row_ids are sorted -- or
+  // every row when the list overflowed its capacity
+  const int64_t* row_ids;
+  const unsigned long long* row_count;
+  int64_t row_cap;
 };
 
 // range / leaf descriptor: lo:11 | cnt:11 | depth:7 | buf:1 | leaf kind:2
@@ -221,9 +227,11 @@ __global__ void __launch_bounds__(RssCfg<U, P, NMAX, DAG, MODE, LAYOUT>::WARPS *
   const int sample = 4 * a;
   const Xform xf = prm.xf;
 
-  const int64_t nrows = prm.seg_count ? min(int64_t(*prm.seg_count), prm.rows) : prm.rows;
-  for (int64_t row = int64_t(blockIdx.x) * Cfg::WARPS + warp; row < nrows;
-       row += int64_t(gridDim.x) * Cfg::WARPS) {
+  const bool listed = prm.row_ids != nullptr && *prm.row_count <= (unsigned long long)prm.row_cap;
+  const int64_t nrows = prm.seg_count ? min(int64_t(*prm.seg_count), prm.rows)
+                                      : (listed ? int64_t(*prm.row_count) : prm.rows);
+  for (int64_t it = int64_t(blockIdx.x) * Cfg::WARPS + warp; it < nrows; it += int64_t(gridDim.x) * Cfg::WARPS) {
+    const int64_t row = listed ? prm.row_ids[it] : it;
     int n = prm.n;
     int64_t base = row * int64_t(prm.n);
     if (prm.seg_ids) {
@@ -1029,6 +1037,31 @@ int launch_rss(const nsg_spec& sp, const void* k_in, void* k_out, const void* p_
   if (sp.kind == NSG_KIND_RSS && layout == LAYOUT_SOA && !seg_ids && (pay == 0 || mode == MODE_UNIQUE) &&
       pksort_covers(n) && !env_flag_set("NSG_RSS_FAITHFUL"))
     return launch_pkrss(k_in, k_out, p_in, p_out, rows, n, key_bytes, pay, sp.rss_sample_seed, xf, st);
+  // REF mode with payloads (typed rows, AoS reference items), 17..256 items:
+  // a row whose keys are all distinct has ONE sorted order, so the packed
+  // sorter produces it; rows with equal keys keep their input order there and
+  // are replayed draw for draw below, from the output, through a device list.
+  PkDefer defer{nullptr, nullptr, 0};
+  void* defer_mem = nullptr;
+  const bool ref_fast = sp.kind == NSG_KIND_RSS && !seg_ids && mode == MODE_REF && pay != 0 && pksort_covers(n) &&
+                        (layout == LAYOUT_SOA || (layout == LAYOUT_AOS16 && key_bytes == 8 && pay == 2)) &&
+                        !env_flag_set("NSG_RSS_FAITHFUL");
+  if (ref_fast) {
+    defer.cap = rows < (int64_t(1) << 18) ? rows : (int64_t(1) << 18);
+    cudaError_t e = cudaMallocAsync(&defer_mem, 16 + size_t(defer.cap) * 8, st);
+    if (e != cudaSuccess) return fail(NSG_ERR_CUDA, "cudaMallocAsync: %s", cudaGetErrorString(e));
+    defer.count = static_cast<unsigned long long*>(defer_mem);
+    defer.ids = reinterpret_cast<int64_t*>(static_cast<unsigned char*>(defer_mem) + 16);
+    e = cudaMemsetAsync(defer_mem, 0, 16, st);
+    if (e != cudaSuccess) return fail(NSG_ERR_CUDA, "memset: %s", cudaGetErrorString(e));
+    if (int rc = launch_pkrss_ref(k_in, k_out, p_in, p_out, rows, n, key_bytes, pay, layout == LAYOUT_AOS16,
+                                  sp.rss_sample_seed, xf, defer, st)) {
+      cudaFreeAsync(defer_mem, st);
+      return rc;
+    }
+    k_in = k_out;  // the listed rows are sorted in place, from the output
+    p_in = p_out;
+  }
   RssParams prm{};
   prm.k_in = k_in;
   prm.k_out = k_out;
@@ -1052,15 +1085,22 @@ int launch_rss(const nsg_spec& sp, const void* k_in, void* k_out, const void* p_
   prm.seg_count = seg_count;
   prm.seg_overflow = seg_overflow;
   prm.big_elsewhere = seg_ids && (pay == 0 || mode == MODE_UNIQUE);
-  const bool per_thread = !seg_ids && n <= 32 && !env_flag_set("NSG_RSS_WARP_ONLY");
+  prm.row_ids = defer.ids;
+  prm.row_count = defer.count;
+  prm.row_cap = defer.cap;
+  const bool per_thread = !seg_ids && !ref_fast && n <= 32 && !env_flag_set("NSG_RSS_WARP_ONLY");
   const RssKernel k = per_thread ? rss_thread_pick(sp.family == 0 ? 0 : 1, key_bytes, pay, mode, layout)
                                  : rss_pick(int(n), sp.family == 0 ? 0 : 1, key_bytes, pay, mode, layout);
   int sms = 0, occ = 0;
-  if (int rc = kernel_residency(k.fn, k.threads, k.smem, &occ, &sms)) return rc;
+  if (int rc = kernel_residency(k.fn, k.threads, k.smem, &occ, &sms)) {
+    if (defer_mem) cudaFreeAsync(defer_mem, st);
+    return rc;
+  }
   const int64_t need = (rows + k.warps - 1) / k.warps;
   const int64_t grid = need < int64_t(sms) * occ ? need : int64_t(sms) * occ;
   void* args[] = {&prm};
   const cudaError_t e = cudaLaunchKernel(k.fn, dim3(unsigned(grid)), dim3(unsigned(k.threads)), args, size_t(k.smem), st);
+  if (defer_mem) cudaFreeAsync(defer_mem, st);
   if (e != cudaSuccess) return fail(NSG_ERR_CUDA, "rss_kernel launch: %s", cudaGetErrorString(e));
   return 0;
 }

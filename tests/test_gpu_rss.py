@@ -170,6 +170,9 @@ def test_rss_thread_and_warp_kernels_agree(mode, torch, monkeypatch):
         keys = rng.integers(0, 5, size=(301, n), dtype=np.uint64)
         refs = np.arange(keys.size, dtype=np.uint64).reshape(keys.shape)
         outs = []
+        # (the packed sorter now serves REF rows of 17..256 items first;
+        # NSG_RSS_FAITHFUL=1 keeps this test on the two draw-for-draw kernels)
+        monkeypatch.setenv("NSG_RSS_FAITHFUL", "1")
         for warp_only in ("0", "1"):
             monkeypatch.setenv("NSG_RSS_WARP_ONLY", warp_only)
             if mode == "ref_items":
@@ -185,3 +188,55 @@ def test_rss_thread_and_warp_kernels_agree(mode, torch, monkeypatch):
             assert np.array_equal(outs[0], exp) and np.array_equal(outs[1], exp), n
         else:
             assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1]), n
+
+
+@pytest.mark.parametrize("n", [20, 96, 256])
+def test_ref_rows_fast_path_and_deferred_rows(n, torch, monkeypatch):
+    """REF-mode items of 17..256 keys: rows with all-distinct keys are sorted by
+    the packed sorter (their order is unique), rows with equal keys keep their
+    input order there and are replayed draw for draw from a device list.  A
+    batch mixing both, against the oracle, and against the draw-for-draw
+    kernel alone (NSG_RSS_FAITHFUL=1)."""
+    from paper_2002_05599_b200 import backend, registry
+    rng = np.random.default_rng(1000 + n)
+    m = 60_000
+    keys = rng.integers(0, 2**64, size=(m, n), dtype=np.uint64)
+    dup = rng.random(m) < 0.05
+    keys[dup, 1] = keys[dup, 0]                      # one equal pair
+    heavy = rng.random(m) < 0.02
+    keys[heavy] = keys[heavy] % np.uint64(3)         # duplicate-heavy rows
+    keys[7] = np.sort(keys[7])
+    refs = rng.integers(0, 2**64, size=(m, n), dtype=np.uint64)
+    spec = registry.spec_rss("332", "SN Best 4CmS")
+    exp = _items(keys, refs)
+    oracle.run_items(exp, kind="rss", family="best", rss_cfg="332", base="net")
+    got = _items(keys, refs)
+    backend.run_sorter_many(spec, got)
+    assert np.array_equal(got, exp)
+    dt = torch.from_numpy(_items(keys, refs).view(np.uint64).reshape(m, n, 2).view(np.int64)).cuda()
+    backend.run_sorter_many(spec, dt)
+    assert np.array_equal(dt.cpu().numpy().view(np.uint64).reshape(m, n * 2).view(oracle.ITEM), exp)
+    monkeypatch.setenv("NSG_RSS_FAITHFUL", "1")
+    slow = _items(keys, refs)
+    backend.run_sorter_many(spec, slow)
+    assert np.array_equal(slow, exp)
+
+
+def test_ref_rows_deferred_list_overflow(torch):
+    """More rows with equal keys than the deferred-row list holds (2^18): the
+    draw-for-draw kernel then replays every row, from the output of the packed
+    sorter (sorted rows and rows left in input order alike)."""
+    from paper_2002_05599_b200 import backend, registry
+    rng = np.random.default_rng(18)
+    m, n = 300_000, 24
+    keys = rng.integers(0, 2**64, size=(m, n), dtype=np.uint64)
+    keys[:, 5] = keys[:, 17]                         # every row has an equal pair
+    keys[::7] %= np.uint64(4)
+    keys[1::1000, 5] += np.uint64(1)                 # a few rows with distinct keys
+    refs = np.arange(m * n, dtype=np.uint64).reshape(m, n)
+    spec = registry.spec_rss("333", "SN BN-L 4CmS")
+    exp = _items(keys, refs)
+    oracle.run_items(exp, kind="rss", family="bn-l", rss_cfg="333", base="net", threads=8)
+    got = _items(keys, refs)
+    backend.run_sorter_many(spec, got)
+    assert np.array_equal(got, exp)

@@ -15,7 +15,9 @@ BASELINE configuration under "workloads" (default `--workloads all`):
   cfg1  2^20 x n=8 uint32, best_08, L2 flushed between reps; a same-box
         device copy of the same bytes is timed beside it as the ceiling;
   cfg3  Register Sample Sort 332 (and the merge sorter) x {uniform, few16,
-        sorted, reverse} x n in {32, 64, 128, 256}, 2^20 int64 rows each;
+        sorted, reverse} x n in {32, 64, 128, 256}, 2^20 int64 rows each, plus
+        the reference-shaped entry (run_sorter_many on AoS (key, ref) items,
+        REF mode) on the uniform rows;
   cfg4  67,108,864 CSR segments (truncated geometric lengths 1..16), f32
         weights descending + u32 ids;
   cfg5  2^28 arrays of 16 uint64 keys + uint64 global index, best_16 UNIQUE,
@@ -749,6 +751,45 @@ def cfg3_inputs(torch, dev, n, rows):
     return (("uniform", uni), ("few16", few), ("sorted", srt), ("reverse", rev))
 
 
+def cfg3_items_cell(torch, dev, x, n, rows, reps, peak):
+    """run_sorter_many(spec_rss("332"), items) on device-resident reference items
+    (16 bytes each: u64 key, u64 ref), checked against the oracle on 512 rows
+    and for key order / ref permutation on all rows."""
+    import oracle
+    from paper_2002_05599_b200 import backend, registry
+    from paper_2002_05599_b200.errors import CorrectnessFailure
+    spec = registry.spec_rss("332")
+    items = torch.empty((rows, n, 2), dtype=torch.int64, device=dev)
+    items[:, :, 0] = x ^ (-2**63)
+    items[:, :, 1] = torch.arange(rows * n, device=dev).view(rows, n)
+    work = torch.empty_like(items)
+    times = []
+    for rep in range(reps + 2):
+        work.copy_(items)
+        torch.cuda._sleep(200_000)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        backend.run_sorter_many(spec, work)
+        e.record()
+        e.synchronize()
+        if rep >= 2:
+            times.append(s.elapsed_time(e))
+    sub = items[:512].cpu().numpy().view(np.uint64)
+    exp = np.empty((512, n), dtype=oracle.ITEM)
+    exp["key"], exp["ref"] = sub[:, :, 0], sub[:, :, 1]
+    oracle.run_items(exp, kind="rss", rss_cfg="332")
+    got = work[:512].cpu().numpy().view(np.uint64)
+    keys_u = work[:, :, 0] ^ (-2**63)  # back to int64 order
+    ok = bool((keys_u[:, 1:] >= keys_u[:, :-1]).all())
+    ok = ok and bool(torch.equal(torch.sort(work[:, :, 1], dim=1).values, items[:, :, 1]))
+    if not ok or not (np.array_equal(got[:, :, 0], exp["key"]) and np.array_equal(got[:, :, 1], exp["ref"])):
+        raise CorrectnessFailure(f"cfg3 items n={n}: parity")
+    blk = rate_block(2 * rows * n * 16, rows, rows * n, float(np.median(times)), float(np.min(times)), peak)
+    blk["api"] = "backend.run_sorter_many(spec_rss('332'), items) -- AoS (u64 key, u64 ref), REF mode, in place"
+    del items, work
+    return blk
+
+
 def wl_cfg3(args, torch, dev, grp, peak, want_cpu):
     import oracle
     from paper_2002_05599_b200 import _lib, batch, registry
@@ -771,6 +812,9 @@ def wl_cfg3(args, torch, dev, grp, peak, want_cpu):
                     raise CorrectnessFailure(f"cfg3 {kind} n={n} {dname}: {bad} bad rows")
                 res["cells"][f"{'rss' if kind == 'rss' else 'merge'}_n{n}_{dname}"] = rate_block(
                     2 * rows * n * 8, rows, rows * n, med, best, peak)
+        # the reference-shaped entry on the same uniform rows: run_sorter_many on
+        # AoS (key ^ 2^63, ref = global index) items, RSS 332 in REF mode, in place
+        res["cells"][f"rss_items_n{n}_uniform"] = cfg3_items_cell(torch, dev, ins[0][1], n, rows, args.reps, peak)
         if want_cpu:
             for dname, x in ins:
                 m = {32: 32768, 64: 16384, 128: 8192, 256: 4096}.get(n, 4096)
@@ -787,7 +831,7 @@ def wl_cfg3(args, torch, dev, grp, peak, want_cpu):
         r = [v["ms_median"] for k, v in cells.items() if k.startswith(f"rss_n{n}_")]
         mg = [v["ms_median"] for k, v in cells.items() if k.startswith(f"merge_n{n}_")]
         res[f"n{n}_rss_over_merge_speed"] = round(float(np.mean(mg) / np.mean(r)), 3)
-    res["min_frac_rss"] = min(v["frac"] for k, v in cells.items() if k.startswith("rss"))
+    res["min_frac_rss"] = min(v["frac"] for k, v in cells.items() if k.startswith("rss_n"))
     return res
 
 

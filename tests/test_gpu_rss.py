@@ -240,3 +240,22 @@ def test_ref_rows_deferred_list_overflow(torch):
     got = _items(keys, refs)
     backend.run_sorter_many(spec, got)
     assert np.array_equal(got, exp)
+
+
+def test_packed_sorters_lane_copy_fallback(torch, monkeypatch):
+    """NSG_PK_NOBULK=1 takes the lane-copy staging of the packed sorters (what
+    unaligned buffers get) through the padded-row and AoS layouts."""
+    from paper_2002_05599_b200 import backend, batch, registry
+    monkeypatch.setenv("NSG_PK_NOBULK", "1")
+    rng = np.random.default_rng(44)
+    for n in (32, 64, 100, 256):
+        keys = rng.integers(-2**63, 2**63 - 1, size=(1501, n), dtype=np.int64)
+        keys[::6] %= 4
+        for kind in ("merge", "rss"):
+            k, _ = batch.sort_rows(torch.from_numpy(keys).cuda(), kind=kind)
+            assert np.array_equal(k.cpu().numpy(), np.sort(keys, axis=1)), (kind, n)
+        items = _items(keys.view(np.uint64), np.arange(keys.size, dtype=np.uint64).reshape(keys.shape))
+        exp = items.copy()
+        oracle.run_items(exp, kind="rss", rss_cfg="332")
+        backend.run_sorter_many(registry.spec_rss("332"), items)
+        assert np.array_equal(items, exp), n

@@ -710,16 +710,26 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
         const int q = ll + L * r;  // q / E folds to (L*r)/E when L <= E
         const uint32_t idx = pr[L <= E ? q + (L * r) / E : q + q / E] & uint32_t(NR - 1);
         NSG_DCHECK(!rowv || int(idx) < n);
-        ok[r] = rk[idx * ST];
-        if constexpr (HAS_P) op[r] = rp[idx * ST];
+        if constexpr (AOS) {  // one 16-byte access per item
+          const ulonglong2 it = reinterpret_cast<const ulonglong2*>(rk)[idx];
+          ok[r] = U(it.x);
+          op[r] = P(it.y);
+        } else {
+          ok[r] = rk[idx];
+          if constexpr (HAS_P) op[r] = rp[idx];
+        }
       }
     }
     __syncwarp();  // every gather is done before the staged rows are overwritten
 #pragma unroll
     for (int r = 0; r < E; ++r) {
       if (FULL || r < rl) {
-        rk[(ll + L * r) * ST] = ok[r];
-        if constexpr (HAS_P) rp[(ll + L * r) * ST] = op[r];
+        if constexpr (AOS) {
+          reinterpret_cast<ulonglong2*>(rk)[ll + L * r] = make_ulonglong2(uint64_t(ok[r]), uint64_t(op[r]));
+        } else {
+          rk[ll + L * r] = ok[r];
+          if constexpr (HAS_P) rp[ll + L * r] = op[r];
+        }
       }
     }
     __syncwarp();

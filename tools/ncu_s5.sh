@@ -26,6 +26,11 @@ for what in "$@"; do
     pkrss64) cap pkrss64_s5 pksort_kernel 1 1 python tools/pk_one.py 64 uniform rss ;;
     pkmrg32) cap pkmrg32_s5 pksort_kernel 1 1 python tools/pk_one.py 32 uniform merge ;;
     pkmrg64) cap pkmrg64_s5 pksort_kernel 1 1 python tools/pk_one.py 64 uniform merge ;;
+    pkref) cap pkref_s5 pksort_kernel 1 1 python tools/ref_probe.py --ns 256 --reps 1 ;;
+    launches)
+      python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --workloads none > $OUT/plain_launch.log 2>&1 && \
+      ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches.csv \
+        python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --workloads none > $OUT/ncu_launch.log 2>&1 ;;
     net7) cap net7_s5 "net_|nettma|netbulk" 4 4 python bench.py --ns 7 --steps 1 --warmup 1 --no-e2e --no-cpu --workloads none ;;
     net10) cap net10_s5 "net_|nettma|netbulk" 4 4 python bench.py --ns 10 --steps 1 --warmup 1 --no-e2e --no-cpu --workloads none ;;
   esac

@@ -25,6 +25,7 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "wsort.cuh"
 
 namespace nsg {
 
@@ -33,6 +34,8 @@ namespace {
 constexpr int kBigThreads = 1024;
 constexpr int kBigSmemBudget = 128 * 1024;
 constexpr int kMergePer = 8;  // outputs per thread per merge step
+constexpr int kWarpV = 8;               // items per lane of a warp-register chunk
+constexpr int kWarpChunk = 32 * kWarpV;  // 256 items
 
 struct BigParams {
   const void* k_in;
@@ -49,6 +52,7 @@ struct BigParams {
   uint32_t* overflow;
   int64_t min_len;  // segment lists: only entries longer than this
   Xform xf;
+  int cap_items;    // shared-memory capacity of THIS launch (power of two <= CAP)
 };
 
 template <class U, class P>
@@ -85,15 +89,15 @@ __device__ __forceinline__ P xp(P q, const Xform& xf) {
 // src already holds order-preserving keys; `ord_out`: leave dst in that space.
 template <class U, class P>
 __device__ void smem_sort(const U* ksrc, const P* psrc, U* kdst, P* pdst, int len, bool ord_in, bool ord_out,
-                          const Xform& xf, unsigned char* smem) {
-  using C = BigCfg<U, P>;
+                          const Xform& xf, unsigned char* smem, int cap) {
   constexpr bool HAS_P = !IsNoPay<P>::value;
+  const int nthr = int(blockDim.x);
   U* sk = reinterpret_cast<U*>(smem);
-  P* sp = reinterpret_cast<P*>(smem + C::CAP * sizeof(U));
-  int np = 2;
+  P* sp = reinterpret_cast<P*>(smem + size_t(cap) * sizeof(U));
+  int np = kWarpChunk;  // at least one warp chunk
   while (np < len) np <<= 1;
-  NSG_DCHECK(np <= C::CAP);
-  for (int i = threadIdx.x; i < np; i += kBigThreads) {
+  NSG_DCHECK(np <= cap);
+  for (int i = threadIdx.x; i < np; i += nthr) {
     if (i < len) {
       sk[i] = ord_in ? ksrc[i] : ord_k<U, P>(ksrc[i], xf);
       if constexpr (HAS_P) sp[i] = ord_in ? psrc[i] : xp<P>(psrc[i], xf);
@@ -103,10 +107,42 @@ __device__ void smem_sort(const U* ksrc, const P* psrc, U* kdst, P* pdst, int le
     }
   }
   __syncthreads();
+  // The bitonic network's stages with partner distance < 256 never leave a
+  // 256-item chunk: a warp runs them in registers (8 items per lane, the
+  // cross-lane ones by shuffle) with no CTA barrier -- the whole sort of a
+  // chunk first (levels k <= 256; odd chunks end descending, stored reversed),
+  // then, per level k >= 512, the stages j >= 256 through shared memory (one
+  // barrier each) and the remaining eight stages again per chunk in registers.
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nchunks = np / kWarpChunk;
+  auto load_chunk = [&](int c, Elem<U, P> (&v)[kWarpV]) {
+#pragma unroll
+    for (int r = 0; r < kWarpV; ++r) {
+      const int i = c * kWarpChunk + lane * kWarpV + r;
+      v[r].k = sk[i];
+      if constexpr (HAS_P) v[r].p = sp[i];
+    }
+  };
+  auto store_chunk = [&](int c, const Elem<U, P> (&v)[kWarpV], bool reversed) {
+#pragma unroll
+    for (int r = 0; r < kWarpV; ++r) {
+      const int q = lane * kWarpV + r;
+      const int i = c * kWarpChunk + (reversed ? kWarpChunk - 1 - q : q);
+      sk[i] = v[r].k;
+      if constexpr (HAS_P) sp[i] = v[r].p;
+    }
+  };
+  for (int c = warp; c < nchunks; c += nthr / 32) {
+    Elem<U, P> v[kWarpV];
+    load_chunk(c, v);
+    bitonic_warp<U, P, kWarpV>(v, lane);
+    store_chunk(c, v, (c & 1) != 0);
+  }
+  __syncthreads();
   const int half = np >> 1;
-  for (int k = 2; k <= np; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int t = threadIdx.x; t < half; t += kBigThreads) {
+  for (int k = 2 * kWarpChunk; k <= np; k <<= 1) {
+    for (int j = k >> 1; j >= kWarpChunk; j >>= 1) {
+      for (int t = threadIdx.x; t < half; t += nthr) {
         const int i = 2 * t - (t & (j - 1));  // low index of the pair (bit j clear)
         const int m = i + j;
         const bool asc = (i & k) == 0;
@@ -128,8 +164,15 @@ __device__ void smem_sort(const U* ksrc, const P* psrc, U* kdst, P* pdst, int le
       }
       __syncthreads();
     }
+    for (int c = warp; c < nchunks; c += nthr / 32) {
+      Elem<U, P> v[kWarpV];
+      load_chunk(c, v);
+      bitonic_warp_tail<U, P, kWarpV>(v, lane, ((c * kWarpChunk) & k) == 0);
+      store_chunk(c, v, false);
+    }
+    __syncthreads();
   }
-  for (int i = threadIdx.x; i < len; i += kBigThreads) {
+  for (int i = threadIdx.x; i < len; i += nthr) {
     kdst[i] = ord_out ? sk[i] : unord_k<U, P>(sk[i], xf);
     if constexpr (HAS_P) pdst[i] = ord_out ? sp[i] : xp<P>(sp[i], xf);
   }
@@ -164,7 +207,7 @@ template <class U, class P>
 __device__ void merge_pass(const U* sk, const P* sp, U* dk, P* dp, int64_t len, int64_t w, bool last,
                            const Xform& xf) {
   constexpr bool HAS_P = !IsNoPay<P>::value;
-  constexpr int64_t CH = int64_t(kBigThreads) * kMergePer;
+  const int64_t CH = int64_t(blockDim.x) * kMergePer;
   for (int64_t c0 = 0; c0 < len; c0 += CH) {
     const int64_t o = c0 + int64_t(threadIdx.x) * kMergePer;  // this thread's first output
     if (o < len) {
@@ -241,7 +284,7 @@ __global__ void __launch_bounds__(kBigThreads, 1) bigsort_kernel(const BigParams
     U* ko = kout + base;
     P* po = HAS_P ? pout + base : pout;
     if (len <= C::CAP) {
-      smem_sort<U, P>(ki, pi, ko, po, int(len), false, false, xf, smem);
+      smem_sort<U, P>(ki, pi, ko, po, int(len), false, false, xf, smem, prm.cap_items);
       continue;
     }
     if (!kscr) {  // no scratch: left unsorted, counted
@@ -257,7 +300,8 @@ __global__ void __launch_bounds__(kBigThreads, 1) bigsort_kernel(const BigParams
     P* p0 = (passes & 1) ? ps : po;
     for (int64_t t0 = 0; t0 < len; t0 += C::CAP) {
       const int tl = int(len - t0 < C::CAP ? len - t0 : C::CAP);
-      smem_sort<U, P>(ki + t0, HAS_P ? pi + t0 : pi, k0 + t0, HAS_P ? p0 + t0 : p0, tl, false, true, xf, smem);
+      smem_sort<U, P>(ki + t0, HAS_P ? pi + t0 : pi, k0 + t0, HAS_P ? p0 + t0 : p0, tl, false, true, xf, smem,
+                      prm.cap_items);
     }
     U* sk = k0;
     P* sp = p0;
@@ -291,15 +335,30 @@ const void* big_pick(int kb, int pay, int* smem, int* cap) {
 }
 
 int launch_big(const BigParams& prm0, int kb, int pay, int64_t grid_items, cudaStream_t st) {
-  int smem = 0, cap = 0;
-  const void* fn = big_pick(kb, pay, &smem, &cap);
+  int smem_max = 0, cap = 0;
+  const void* fn = big_pick(kb, pay, &smem_max, &cap);
   int sms = 0, occ = 0;
-  if (int rc = kernel_residency(fn, kBigThreads, smem, &occ, &sms)) return rc;
+  if (int rc = kernel_residency(fn, kBigThreads, smem_max, &occ, &sms)) return rc;  // (sets the smem attribute)
+  // Rows of one length <= CAP: the CTA and its shared memory are sized to the
+  // row (8 items per thread, 256..1024 threads), so several rows are resident
+  // per SM and every warp owns a 256-item register chunk.  Segment lists and
+  // rows above CAP keep the full-size CTA.
+  BigParams prm = prm0;
+  int threads = kBigThreads, smem = smem_max;
+  prm.cap_items = cap;
+  if (!prm.seg_ids && prm.n <= cap) {
+    int np = kWarpChunk;
+    while (np < prm.n) np <<= 1;
+    prm.cap_items = np;
+    smem = int(int64_t(smem_max) * np / cap);
+    threads = np / kWarpV < 256 ? 256 : (np / kWarpV > kBigThreads ? kBigThreads : np / kWarpV);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, size_t(smem)) != cudaSuccess || occ < 1)
+      return fail(NSG_ERR_CUDA, "bigsort_kernel cannot be resident (%d threads, %d B)", threads, smem);
+  }
   const int64_t grid = grid_items < int64_t(sms) * occ ? grid_items : int64_t(sms) * occ;
   if (grid <= 0) return 0;
-  BigParams prm = prm0;
   void* args[] = {&prm};
-  const cudaError_t e = cudaLaunchKernel(fn, dim3(unsigned(grid)), dim3(kBigThreads), args, size_t(smem), st);
+  const cudaError_t e = cudaLaunchKernel(fn, dim3(unsigned(grid)), dim3(unsigned(threads)), args, size_t(smem), st);
   if (e != cudaSuccess) return fail(NSG_ERR_CUDA, "bigsort_kernel launch: %s", cudaGetErrorString(e));
   return 0;
 }

@@ -34,7 +34,8 @@ int launch_rss_segment_list(const nsg_spec& sp, const uint32_t* offsets, const u
                             const void* pay_in, void* pay_out, cudaStream_t st);
 
 // pksort.cu (packed-key warp sorter: merge kind, keys-only / UNIQUE rows of 17..256 items)
-bool pksort_covers(int64_t n);
+bool pksort_covers(int64_t n);      // merge phase: 17..512 items
+bool pksort_rss_covers(int64_t n);  // RSS phase: 17..256 items
 int launch_pksort(const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows, int64_t n,
                   int key_bytes, int pay, const Xform& xf, cudaStream_t st);
 // the same skeleton with one Register Sample Sort level as the sort phase

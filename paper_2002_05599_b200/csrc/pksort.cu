@@ -277,12 +277,12 @@ __device__ __forceinline__ bool item_lt(U bk, const P& bp, U ak, const P& ap) {
 }
 
 // Exact in-place re-sort of one staged row (raw keys) by the whole warp.
-template <class U, class P>
+template <class U, class P, int V>
 __device__ __noinline__ void pk_exact_row(U* rk, P* rp, int n, const Xform xf, int lane, int st) {
-  Elem<U, P> v[8];
+  Elem<U, P> v[V];  // V items per lane: 8 up to 256-item rows, 16 above
 #pragma unroll
-  for (int r = 0; r < 8; ++r) {
-    const int i = lane * 8 + r;
+  for (int r = 0; r < V; ++r) {
+    const int i = lane * V + r;
     if (i < n) {
       v[r].k = xf.active ? to_ord<U>(rk[i * st], xf) : rk[i * st];
       if constexpr (!IsNoPay<P>::value) v[r].p = xf.active ? P(rp[i * st] ^ P(xf.pdesc)) : rp[i * st];
@@ -292,10 +292,10 @@ __device__ __noinline__ void pk_exact_row(U* rk, P* rp, int n, const Xform xf, i
     }
   }
   __syncwarp();
-  bitonic_warp<U, P, 8>(v, lane);
+  bitonic_warp<U, P, V>(v, lane);
 #pragma unroll
-  for (int r = 0; r < 8; ++r) {
-    const int i = lane * 8 + r;
+  for (int r = 0; r < V; ++r) {
+    const int i = lane * V + r;
     if (i < n) {
       rk[i * st] = xf.active ? from_ord<U>(v[r].k, xf) : v[r].k;
       if constexpr (!IsNoPay<P>::value) rp[i * st] = xf.active ? P(v[r].p ^ P(xf.pdesc)) : v[r].p;
@@ -820,7 +820,7 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
       const int gi = __ffs(int(bad_rows)) - 1;
       bad_rows &= bad_rows - 1;
       if (lane == 0) atomicAdd(&g_pk_fallback_rows, 1ull);
-      pk_exact_row<U, P>(fk + gi * rs * ST, fp + gi * rs * ST, n, xf, lane, ST);
+      pk_exact_row<U, P, (NR > 256 ? 16 : 8)>(fk + gi * rs * ST, fp + gi * rs * ST, n, xf, lane, ST);
     }
 
     // ---- 6. store -----------------------------------------------------------
@@ -888,6 +888,8 @@ const void* pk_fn(int lognr, bool full, bool rss, int* smem) {
     NSG_PK_CASE(7)
     NSG_PK_CASE(8)
 #undef NSG_PK_CASE
+    case 9:  // 257..512 items: one row per warp, merge phase only (the RSS phase's 8-word blocks stop at 256)
+      return rss ? nullptr : pk_fn_lg<U, P, 9, false>(full, smem);
     default: return nullptr;
   }
 }
@@ -916,12 +918,14 @@ const void* pk_pick(int kb, int pay, int lognr, bool full, bool rss, int* smem) 
 
 }  // namespace
 
-bool pksort_covers(int64_t n) { return n >= 17 && n <= 256; }
+bool pksort_covers(int64_t n) { return n >= 17 && n <= 512; }       // merge phase
+bool pksort_rss_covers(int64_t n) { return n >= 17 && n <= 256; }   // RSS phase (8-word blocks, 32 lanes)
 
 static int launch_pk(const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows, int64_t n,
                      int key_bytes, int pay, const Xform& xf, bool rss, uint32_t seed, cudaStream_t st,
                      bool aos = false, const PkDefer* defer = nullptr) {
-  if (!pksort_covers(n)) return fail(NSG_ERR_SPEC, "packed warp sorters cover 17..256 items, got %lld", (long long)n);
+  if (!(rss ? pksort_rss_covers(n) : pksort_covers(n)))
+    return fail(NSG_ERR_SPEC, "packed warp sorters cover 17..%d items, got %lld", rss ? 256 : 512, (long long)n);
   if (rows <= 0) return 0;
   int lognr = 5;
   while ((1 << lognr) < n) ++lognr;

@@ -1035,15 +1035,20 @@ int launch_rss(const nsg_spec& sp, const void* k_in, void* k_out, const void* p_
   // kernels below stay for REF mode (payload order under key ties), AoS
   // items, CSR segment lists and NSG_RSS_FAITHFUL=1.
   if (sp.kind == NSG_KIND_RSS && layout == LAYOUT_SOA && !seg_ids && (pay == 0 || mode == MODE_UNIQUE) &&
-      pksort_covers(n) && !env_flag_set("NSG_RSS_FAITHFUL"))
-    return launch_pkrss(k_in, k_out, p_in, p_out, rows, n, key_bytes, pay, sp.rss_sample_seed, xf, st);
+      pksort_covers(n) && !env_flag_set("NSG_RSS_FAITHFUL")) {
+    if (pksort_rss_covers(n))
+      return launch_pkrss(k_in, k_out, p_in, p_out, rows, n, key_bytes, pay, sp.rss_sample_seed, xf, st);
+    // 257..512 items: the same packed kernel with its merge phase (one row
+    // per warp; the RSS phase's 8-word blocks stop at 256 items)
+    return launch_pksort(k_in, k_out, p_in, p_out, rows, n, key_bytes, pay, xf, st);
+  }
   // REF mode with payloads (typed rows, AoS reference items), 17..256 items:
   // a row whose keys are all distinct has ONE sorted order, so the packed
   // sorter produces it; rows with equal keys keep their input order there and
   // are replayed draw for draw below, from the output, through a device list.
   PkDefer defer{nullptr, nullptr, 0};
   void* defer_mem = nullptr;
-  const bool ref_fast = sp.kind == NSG_KIND_RSS && !seg_ids && mode == MODE_REF && pay != 0 && pksort_covers(n) &&
+  const bool ref_fast = sp.kind == NSG_KIND_RSS && !seg_ids && mode == MODE_REF && pay != 0 && pksort_rss_covers(n) &&
                         (layout == LAYOUT_SOA || (layout == LAYOUT_AOS16 && key_bytes == 8 && pay == 2)) &&
                         !env_flag_set("NSG_RSS_FAITHFUL");
   if (ref_fast) {

@@ -77,4 +77,32 @@ __device__ __forceinline__ void bitonic_warp(Elem<U, P> (&v)[E], int lane) {
   }
 }
 
+// The last log2(32*E) stages of one bitonic level (partner distances 16*E ..
+// 1) over the warp's 32*E items: a bitonic sequence becomes sorted, ascending
+// or descending by `asc`.
+template <class U, class P, int E>
+__device__ __forceinline__ void bitonic_warp_tail(Elem<U, P> (&v)[E], int lane, bool asc) {
+#pragma unroll
+  for (int lm = 16; lm > 0; lm >>= 1) {
+    const bool low = (lane & lm) == 0;
+    const bool keep_min = asc == low;
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+      Elem<U, P> o;
+      o.k = shfl_x(v[r].k, lm);
+      if constexpr (!IsNoPay<P>::value) o.p = shfl_x(v[r].p, lm);
+      const bool use_o = keep_min ? e_less(o, v[r]) : e_less(v[r], o);
+      v[r].k = use_o ? o.k : v[r].k;
+      if constexpr (!IsNoPay<P>::value) v[r].p = use_o ? o.p : v[r].p;
+    }
+  }
+#pragma unroll
+  for (int j = E >> 1; j > 0; j >>= 1) {
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+      if ((r & j) == 0) cx_dir(v[r], v[r | j], asc);
+    }
+  }
+}
+
 }  // namespace nsg

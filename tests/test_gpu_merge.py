@@ -47,7 +47,7 @@ def test_merge_keys_only(n, kdt, torch):
         assert np.array_equal(k.cpu().numpy().view(keys.dtype), exp), (n, kdt, desc)
 
 
-@pytest.mark.parametrize("n", [20, 32, 64, 96, 128, 256, 700])
+@pytest.mark.parametrize("n", [20, 32, 64, 96, 128, 256, 300, 512, 700])
 @pytest.mark.parametrize("pdt", ["uint32", "uint64"])
 def test_merge_unique_payload_vs_oracle(n, pdt, torch):
     from paper_2002_05599_b200 import batch

@@ -115,7 +115,7 @@ def test_insertion_kind_is_stable(torch):
 def test_rss_typed_rows_vs_oracle(kdt, pdt, torch):
     from paper_2002_05599_b200 import batch
     rng = np.random.default_rng(7)
-    for n in (32, 64, 128, 256):
+    for n in (32, 64, 128, 256, 300, 512):  # 257..512: the packed kernel's merge phase (keys-only / UNIQUE)
         for tie in (["unique"] if pdt is None else ["unique", "ref"]):
             for desc in (False, True):
                 if kdt.startswith("float"):

@@ -867,13 +867,12 @@ const void* pk_fn_lg(bool full, int* smem) {
     return full ? reinterpret_cast<const void*>(&pksort_kernel<U, P, LG, E, true, PHF, PAD, AOS>)
                 : reinterpret_cast<const void*>(&pksort_kernel<U, P, LG, E, false, PH, false, AOS>);
   } else {
-    static_assert(!AOS, "AoS items take the RSS phase");
     constexpr bool PAD = PkPad<U, P, LG, NSG_PK_E>::value;
     using PH = PhaseBitonic<LG, NSG_PK_E>;
     constexpr int PADE = PAD ? (1 << LG) / NSG_PK_E : 0;
-    *smem = full ? PkCfg<U, P, LG, NSG_PK_E, 0, PADE>::CTA_SMEM : PkCfg<U, P, LG, NSG_PK_E, 0>::CTA_SMEM;
-    return full ? reinterpret_cast<const void*>(&pksort_kernel<U, P, LG, NSG_PK_E, true, PH, PAD>)
-                : reinterpret_cast<const void*>(&pksort_kernel<U, P, LG, NSG_PK_E, false, PH>);
+    *smem = full ? PkCfg<U, P, LG, NSG_PK_E, 0, PADE, AOS>::CTA_SMEM : PkCfg<U, P, LG, NSG_PK_E, 0, 0, AOS>::CTA_SMEM;
+    return full ? reinterpret_cast<const void*>(&pksort_kernel<U, P, LG, NSG_PK_E, true, PH, PAD, AOS>)
+                : reinterpret_cast<const void*>(&pksort_kernel<U, P, LG, NSG_PK_E, false, PH, false, AOS>);
   }
 }
 
@@ -894,9 +893,10 @@ const void* pk_fn(int lognr, bool full, bool rss, int* smem) {
   }
 }
 
-// reference items (AoS, u64 key + u64 ref): RSS phase only
+// reference items (AoS, u64 key + u64 ref): RSS phase up to 256 items, merge phase for 257..512
 const void* pk_pick_aos(int lognr, bool full, int* smem) {
   switch (lognr) {
+    case 9: return pk_fn_lg<uint64_t, uint64_t, 9, false, true>(full, smem);
     case 5: return pk_fn_lg<uint64_t, uint64_t, 5, true, true>(full, smem);
     case 6: return pk_fn_lg<uint64_t, uint64_t, 6, true, true>(full, smem);
     case 7: return pk_fn_lg<uint64_t, uint64_t, 7, true, true>(full, smem);
@@ -967,7 +967,8 @@ int launch_pkrss(const void* k_in, void* k_out, const void* p_in, void* p_out, i
 int launch_pkrss_ref(const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows, int64_t n,
                      int key_bytes, int pay, bool aos, uint32_t seed, const Xform& xf, const PkDefer& defer,
                      cudaStream_t st) {
-  return launch_pk(k_in, k_out, p_in, p_out, rows, n, key_bytes, pay, xf, true, seed, st, aos, &defer);
+  // (257..512 items: the merge phase; a distinct-key row has one sorted order either way)
+  return launch_pk(k_in, k_out, p_in, p_out, rows, n, key_bytes, pay, xf, pksort_rss_covers(n), seed, st, aos, &defer);
 }
 
 unsigned long long pksort_fallback_rows(bool reset) {

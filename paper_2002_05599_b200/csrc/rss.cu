@@ -1048,7 +1048,7 @@ int launch_rss(const nsg_spec& sp, const void* k_in, void* k_out, const void* p_
   // are replayed draw for draw below, from the output, through a device list.
   PkDefer defer{nullptr, nullptr, 0};
   void* defer_mem = nullptr;
-  const bool ref_fast = sp.kind == NSG_KIND_RSS && !seg_ids && mode == MODE_REF && pay != 0 && pksort_rss_covers(n) &&
+  const bool ref_fast = sp.kind == NSG_KIND_RSS && !seg_ids && mode == MODE_REF && pay != 0 && pksort_covers(n) &&
                         (layout == LAYOUT_SOA || (layout == LAYOUT_AOS16 && key_bytes == 8 && pay == 2)) &&
                         !env_flag_set("NSG_RSS_FAITHFUL");
   if (ref_fast) {

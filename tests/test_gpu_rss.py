@@ -190,7 +190,7 @@ def test_rss_thread_and_warp_kernels_agree(mode, torch, monkeypatch):
             assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1]), n
 
 
-@pytest.mark.parametrize("n", [20, 96, 256])
+@pytest.mark.parametrize("n", [20, 96, 256, 300, 512])
 def test_ref_rows_fast_path_and_deferred_rows(n, torch, monkeypatch):
     """REF-mode items of 17..256 keys: rows with all-distinct keys are sorted by
     the packed sorter (their order is unique), rows with equal keys keep their

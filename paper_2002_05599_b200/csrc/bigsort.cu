@@ -23,6 +23,8 @@
 // kernel takes the rest) and counts those above CAP as overflow.
 #include <cuda_runtime.h>
 
+#include <mutex>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "wsort.cuh"
@@ -316,6 +318,138 @@ __global__ void __launch_bounds__(kBigThreads, 1) bigsort_kernel(const BigParams
   }
 }
 
+// ---------------------------------------------------------------------------
+// Rows of 513 .. midsort_cap items.  pksort.cu has sorted every 512-item chunk
+// of the row (packed 32-bit words, warp registers); one CTA per row finishes
+// it here: the row is copied into shared memory, merge-path passes double the
+// run length between two shared buffers, and the last pass writes the output.
+// Values stay in their own representation; the order transform is applied
+// inside the comparisons only.
+// ---------------------------------------------------------------------------
+constexpr int kMidThreads = 256;   // rows up to 2048 items; kMidThreadsBig above
+constexpr int kMidThreadsBig = 1024;
+constexpr int kMidRun = 512;
+constexpr int kMidBytes = 80 * 1024;  // one buffer: n * (key + payload bytes)
+
+struct MidParams {
+  void* k;   // in place: chunk-sorted rows in, sorted rows out
+  void* p;
+  int64_t rows, n;
+  Xform xf;
+};
+
+template <class U, class P>
+__device__ __forceinline__ bool mid_lt(U bk, const P& bp, U ak, const P& ap, const Xform& xf) {
+  if constexpr (IsNoPay<P>::value) {
+    return xf.active ? key_lt(to_ord<U>(bk, xf), to_ord<U>(ak, xf)) : key_lt(bk, ak);
+  } else {
+    return xf.active ? lex_lt(to_ord<U>(bk, xf), P(bp ^ P(xf.pdesc)), to_ord<U>(ak, xf), P(ap ^ P(xf.pdesc)))
+                     : lex_lt(bk, bp, ak, ap);
+  }
+}
+
+// runs of `w` items of src merged pairwise into dst (either may be shared or global memory)
+template <class U, class P>
+__device__ void mid_pass(const U* sk, const P* sp, U* dk, P* dp, int len, int w, const Xform& xf) {
+  constexpr bool HAS_P = !IsNoPay<P>::value;
+  const int CH = int(blockDim.x) * kMergePer;
+  for (int c0 = 0; c0 < len; c0 += CH) {
+    const int o = c0 + int(threadIdx.x) * kMergePer;  // this thread's first output
+    if (o < len) {
+      const int r0 = o / (2 * w) * (2 * w);  // its run pair
+      const int na = (r0 + w < len ? r0 + w : len) - r0;
+      const int nb = (r0 + 2 * w < len ? r0 + 2 * w : len) - (r0 + na);
+      const U* ak = sk + r0;
+      const U* bk = sk + r0 + na;
+      const P* ap = HAS_P ? sp + r0 : sp;
+      const P* bp = HAS_P ? sp + r0 + na : sp;
+      const int d = o - r0;
+      // merge-path split: how many of the first d outputs come from A (A first on ties)
+      int lo = d > nb ? d - nb : 0, hi = d < na ? d : na;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        P pa{}, pb{};
+        if constexpr (HAS_P) {
+          pa = ap[mid];
+          pb = bp[d - 1 - mid];
+        }
+        if (!mid_lt<U, P>(bk[d - 1 - mid], pb, ak[mid], pa, xf)) lo = mid + 1; else hi = mid;
+      }
+      int ai = lo, bi = d - lo;
+      NSG_DCHECK(ai >= 0 && ai <= na && bi >= 0 && bi <= nb);
+      U ka = U(0), kb = U(0);
+      P pa{}, pb{};
+      if (ai < na) { ka = ak[ai]; if constexpr (HAS_P) pa = ap[ai]; }
+      if (bi < nb) { kb = bk[bi]; if constexpr (HAS_P) pb = bp[bi]; }
+      const int end = r0 + na + nb;
+#pragma unroll
+      for (int q = 0; q < kMergePer; ++q) {
+        if (o + q < end) {
+          const bool take_a = bi >= nb || (ai < na && !mid_lt<U, P>(kb, pb, ka, pa, xf));
+          dk[o + q] = take_a ? ka : kb;
+          if constexpr (HAS_P) dp[o + q] = take_a ? pa : pb;
+          if (take_a) {
+            ++ai;
+            if (ai < na) { ka = ak[ai]; if constexpr (HAS_P) pa = ap[ai]; }
+          } else {
+            ++bi;
+            if (bi < nb) { kb = bk[bi]; if constexpr (HAS_P) pb = bp[bi]; }
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+template <class U, class P, int T>
+__global__ void __launch_bounds__(T) rowmerge_kernel(const MidParams prm) {
+  constexpr bool HAS_P = !IsNoPay<P>::value;
+  constexpr int PB = PayBytes<P>::value;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = int(prm.n);
+  const size_t kreg = (size_t(n) * sizeof(U) + 15) / 16 * 16, preg = (size_t(n) * PB + 15) / 16 * 16;
+  U* ak = reinterpret_cast<U*>(smem);
+  P* ap = reinterpret_cast<P*>(smem + kreg);
+  U* bk = reinterpret_cast<U*>(smem + kreg + preg);
+  P* bp = reinterpret_cast<P*>(smem + 2 * kreg + preg);
+  for (int64_t row = blockIdx.x; row < prm.rows; row += gridDim.x) {
+    U* gk = static_cast<U*>(prm.k) + row * prm.n;
+    P* gp = HAS_P ? static_cast<P*>(prm.p) + row * prm.n : static_cast<P*>(prm.p);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      ak[i] = gk[i];
+      if constexpr (HAS_P) ap[i] = gp[i];
+    }
+    __syncthreads();
+    const U* sk = ak;
+    const P* sp = ap;
+    for (int w = kMidRun; w < n; w <<= 1) {
+      const bool last = 2 * w >= n;
+      U* dk = last ? gk : (sk == ak ? bk : ak);
+      P* dp = last ? gp : (sk == ak ? bp : ap);
+      mid_pass<U, P>(sk, sp, dk, dp, n, w, prm.xf);
+      sk = dk;
+      sp = dp;
+    }
+  }
+}
+
+template <class U, class P>
+const void* mid_fn(bool big) {
+  return big ? reinterpret_cast<const void*>(&rowmerge_kernel<U, P, kMidThreadsBig>)
+             : reinterpret_cast<const void*>(&rowmerge_kernel<U, P, kMidThreads>);
+}
+const void* mid_pick(int kb, int pay, bool big) {
+  if (kb == 4) {
+    if (pay == 0) return mid_fn<uint32_t, NoPay>(big);
+    if (pay == 1) return mid_fn<uint32_t, uint32_t>(big);
+    return mid_fn<uint32_t, uint64_t>(big);
+  }
+  if (pay == 0) return mid_fn<uint64_t, NoPay>(big);
+  if (pay == 1) return mid_fn<uint64_t, uint32_t>(big);
+  return mid_fn<uint64_t, uint64_t>(big);
+}
+
 template <class U, class P>
 const void* big_fn(int* smem, int* cap) {
   *smem = BigCfg<U, P>::SMEM;
@@ -364,6 +498,43 @@ int launch_big(const BigParams& prm0, int kb, int pay, int64_t grid_items, cudaS
 }
 
 }  // namespace
+
+int64_t midsort_cap(int key_bytes, int pay) {
+  const int eb = key_bytes + (pay == 0 ? 0 : pay == 1 ? 4 : 8);
+  return kMidBytes / eb;
+}
+
+int launch_midsort_rows(const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows, int64_t n,
+                        int key_bytes, int pay, const Xform& xf, cudaStream_t st) {
+  if (rows <= 0) return 0;
+  if (n <= kMidRun || n > midsort_cap(key_bytes, pay))
+    return fail(NSG_ERR_SPEC, "midsort covers %d..%lld items", kMidRun + 1, (long long)midsort_cap(key_bytes, pay));
+  if (int rc = launch_pksort_chunks(k_in, k_out, p_in, p_out, rows, n, key_bytes, pay, xf, st)) return rc;
+  const int pb = pay == 0 ? 0 : pay == 1 ? 4 : 8;
+  const size_t kreg = (size_t(n) * key_bytes + 15) / 16 * 16, preg = (size_t(n) * pb + 15) / 16 * 16;
+  const bool two = n > 2 * kMidRun;  // more than one pass: a second buffer
+  const size_t smem = (kreg + preg) * (two ? 2 : 1);
+  const bool big = n > 2048;
+  const int threads = big ? kMidThreadsBig : kMidThreads;
+  const void* fn = mid_pick(key_bytes, pay, big);
+  static std::mutex mu;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kMidBytes + 64) != cudaSuccess)
+      return fail(NSG_ERR_CUDA, "rowmerge_kernel: shared memory attribute");
+  }
+  int dev = 0, sms = 0, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem) != cudaSuccess || occ < 1)
+    return fail(NSG_ERR_CUDA, "rowmerge_kernel cannot be resident (%zu B)", smem);
+  const int64_t grid = rows < int64_t(sms) * occ ? rows : int64_t(sms) * occ;
+  MidParams prm{k_out, p_out, rows, n, xf};
+  void* args[] = {&prm};
+  const cudaError_t e = cudaLaunchKernel(fn, dim3(unsigned(grid)), dim3(unsigned(threads)), args, smem, st);
+  if (e != cudaSuccess) return fail(NSG_ERR_CUDA, "rowmerge_kernel launch: %s", cudaGetErrorString(e));
+  return 0;
+}
 
 int64_t bigsort_cap(int key_bytes, int pay) {
   int smem = 0, cap = 0;

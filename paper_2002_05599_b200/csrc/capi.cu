@@ -244,6 +244,9 @@ int nsg_sort_rows(const nsg_spec* sp, const void* keys_in, void* keys_out, const
     const bool one_lane32 = n == 32 && sp->payload_dtype == NSG_PAY_NONE && !env_flag("NSG_MERGE_PK32");
     if (pksort_covers(n) && !one_lane32 && !env_flag("NSG_MERGE_LEGACY"))  // packed 32-bit words, TMA-staged groups
       return launch_pksort(keys_in, keys_out, pay_in, pay_out, rows, n, kb, sp->payload_dtype, make_xform(*sp), st);
+    // 513 .. midsort_cap items: packed-sorter chunks + merge-path passes in shared memory
+    if (n > 512 && n <= midsort_cap(kb, sp->payload_dtype) && !env_flag("NSG_MERGE_LEGACY"))
+      return launch_midsort_rows(keys_in, keys_out, pay_in, pay_out, rows, n, kb, sp->payload_dtype, make_xform(*sp), st);
     int g = 0;
     const KernelInfo mk = merge_lookup(int(n), kb, sp->payload_dtype, &g);
     if (mk.fn) {  // G lanes per row: sub-row networks + cross-lane bitonic merge

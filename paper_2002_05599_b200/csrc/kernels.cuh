@@ -54,10 +54,18 @@ struct PkDefer {
 int launch_pkrss_ref(const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows, int64_t n,
                      int key_bytes, int pay, bool aos, uint32_t seed, const Xform& xf, const PkDefer& defer,
                      cudaStream_t st);
+// every 512-item chunk (and the shorter tail) of every row sorted in place in the output
+int launch_pksort_chunks(const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows, int64_t n,
+                         int key_bytes, int pay, const Xform& xf, cudaStream_t st);
 unsigned long long pksort_fallback_rows(bool reset);
 
 // bigsort.cu (rows / segments above 1024 items, keys-only / UNIQUE)
 int64_t bigsort_cap(int key_bytes, int pay);
+// rows of 513..midsort_cap items (keys-only / UNIQUE): packed-sorter chunks +
+// merge-path passes in shared memory, one CTA per row
+int64_t midsort_cap(int key_bytes, int pay);
+int launch_midsort_rows(const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows, int64_t n,
+                        int key_bytes, int pay, const Xform& xf, cudaStream_t st);
 int launch_bigsort_rows(const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows, int64_t n,
                         int key_bytes, int pay, const Xform& xf, cudaStream_t st);
 int launch_bigsort_segment_list(const uint32_t* offsets, const uint32_t* ids, const uint32_t* count,

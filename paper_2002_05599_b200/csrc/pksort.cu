@@ -74,6 +74,12 @@ struct PkParams {
   unsigned long long* defer_count;
   int64_t* defer_ids;
   int64_t defer_cap;
+  // chunk mode (rows above 512 items, one row per group only): group grp is
+  // chunk grp % cpr of outer row grp / cpr, at outer_stride items per outer
+  // row plus first_off; cpr == 0: plain contiguous rows
+  int cpr;
+  int64_t outer_stride;
+  int64_t first_off;
 };
 
 __host__ __device__ constexpr int pk_ilog2(int x) { return x <= 1 ? 0 : 1 + pk_ilog2(x >> 1); }
@@ -559,6 +565,11 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
   }
   __syncwarp();
 
+  auto base_of = [&](int64_t grp) -> int64_t {  // first item of the group
+    if (R == 1 && prm.cpr > 0)
+      return (grp / prm.cpr) * prm.outer_stride + (grp % prm.cpr) * int64_t(n) + prm.first_off;
+    return grp * R * int64_t(n);
+  };
   auto rows_in = [&](int64_t grp) -> int {
     const int64_t left = rows - grp * R;
     return left < R ? int(left) : R;
@@ -571,7 +582,7 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
     const int rin = rows_in(grp);
     if constexpr (PAD) {  // one bulk copy per row, issued by the first rin lanes at once
       if (bulk_ok(rin)) {
-        const int64_t base = grp * R * int64_t(n);
+        const int64_t base = base_of(grp);
         if (lane == 0) mbar_expect_tx(&bar[b], unsigned(rin * n * (int(sizeof(U)) + C::PB)));
         __syncwarp();
         if (lane < rin) {
@@ -584,7 +595,7 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
       return;
     }
     if (lane == 0 && bulk_ok(rin)) {
-      const int64_t base = grp * R * int64_t(n);
+      const int64_t base = base_of(grp);
       const unsigned kbytes = unsigned(rin * n * int(sizeof(U)) * ST);
       const unsigned pbytes = AOS ? 0u : unsigned(rin * n * C::PB);
       mbar_expect_tx(&bar[b], kbytes + pbytes);
@@ -612,7 +623,7 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
     P* fp = AOS ? reinterpret_cast<P*>(fk) + 1 : pbuf + b * W;
     const int rin = rows_in(grp);
     const int cnt = rin * n;
-    const int64_t base = grp * R * int64_t(n);
+    const int64_t base = base_of(grp);
     const bool bk = bulk_ok(rin);
     if (bk) {
       mbar_wait_parity(&bar[b], (phases >> b) & 1u);
@@ -921,23 +932,35 @@ const void* pk_pick(int kb, int pay, int lognr, bool full, bool rss, int* smem) 
 bool pksort_covers(int64_t n) { return n >= 17 && n <= 512; }       // merge phase
 bool pksort_rss_covers(int64_t n) { return n >= 17 && n <= 256; }   // RSS phase (8-word blocks, 32 lanes)
 
+struct PkChunks {  // chunk mode of launch_pk (see PkParams::cpr)
+  int cpr;
+  int64_t outer_stride, first_off;
+  int lognr;  // forced row class (tails shorter than the chunk keep the one-row-per-warp kernel)
+};
+
 static int launch_pk(const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows, int64_t n,
                      int key_bytes, int pay, const Xform& xf, bool rss, uint32_t seed, cudaStream_t st,
-                     bool aos = false, const PkDefer* defer = nullptr) {
-  if (!(rss ? pksort_rss_covers(n) : pksort_covers(n)))
+                     bool aos = false, const PkDefer* defer = nullptr, const PkChunks* chunks = nullptr) {
+  if (!(rss ? pksort_rss_covers(n) : pksort_covers(n)) && !(chunks && n >= 1 && n <= 512))
     return fail(NSG_ERR_SPEC, "packed warp sorters cover 17..%d items, got %lld", rss ? 256 : 512, (long long)n);
   if (rows <= 0) return 0;
   int lognr = 5;
   while ((1 << lognr) < n) ++lognr;
+  if (chunks) lognr = chunks->lognr;
   int smem = 0;
   const bool full = n == (int64_t(1) << lognr);
   const void* fn = aos ? pk_pick_aos(lognr, full, &smem) : pk_pick(key_bytes, pay, lognr, full, rss, &smem);
   if (!fn) return fail(NSG_ERR_SPEC, "no packed warp sorter for this configuration");
   const auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  const bool bulk =
-      al(k_in) && al(k_out) && (pay == 0 || aos || (al(p_in) && al(p_out))) && !env_flag("NSG_PK_NOBULK");
+  bool bulk = al(k_in) && al(k_out) && (pay == 0 || aos || (al(p_in) && al(p_out))) && !env_flag("NSG_PK_NOBULK");
+  if (chunks) {  // every chunk must start 16-byte aligned in each region
+    const int pb = pay == 0 ? 0 : pay == 1 ? 4 : 8;
+    bulk = bulk && (chunks->outer_stride * key_bytes) % 16 == 0 && (chunks->first_off * key_bytes) % 16 == 0 &&
+           (chunks->outer_stride * pb) % 16 == 0 && (chunks->first_off * pb) % 16 == 0;
+  }
   PkParams prm{k_in, k_out, p_in, p_out, rows, int(n), bulk ? 1 : 0, 1u, 0xffffffffu, seed == 0 ? 1u : seed, xf,
-               defer ? 1 : 0, defer ? defer->count : nullptr, defer ? defer->ids : nullptr, defer ? defer->cap : 0};
+               defer ? 1 : 0, defer ? defer->count : nullptr, defer ? defer->ids : nullptr, defer ? defer->cap : 0,
+               chunks ? chunks->cpr : 0, chunks ? chunks->outer_stride : 0, chunks ? chunks->first_off : 0};
   int sms = 0, occ = 0;
   constexpr int threads = NSG_PK_WARPS * 32;
   if (int rc = kernel_residency(fn, threads, smem, &occ, &sms)) return rc;
@@ -969,6 +992,27 @@ int launch_pkrss_ref(const void* k_in, void* k_out, const void* p_in, void* p_ou
                      cudaStream_t st) {
   // (257..512 items: the merge phase; a distinct-key row has one sorted order either way)
   return launch_pk(k_in, k_out, p_in, p_out, rows, n, key_bytes, pay, xf, pksort_rss_covers(n), seed, st, aos, &defer);
+}
+
+// Rows of more than 512 items: every 512-item chunk of every row sorted in
+// place in the output (the merge-path passes of bigsort.cu finish the rows).
+// Full chunks in one launch; the rows' tails (n % 512 items, if any) in a
+// second one with the same one-row-per-warp kernel.
+int launch_pksort_chunks(const void* k_in, void* k_out, const void* p_in, void* p_out, int64_t rows, int64_t n,
+                         int key_bytes, int pay, const Xform& xf, cudaStream_t st) {
+  constexpr int CH = 512;
+  const int cpr = int(n / CH);
+  const int tail = int(n % CH);
+  if (cpr > 0) {
+    const PkChunks c{cpr, n, 0, 9};
+    if (int rc = launch_pk(k_in, k_out, p_in, p_out, rows * cpr, CH, key_bytes, pay, xf, false, 0u, st, false, nullptr, &c))
+      return rc;
+  }
+  if (tail > 0) {
+    const PkChunks c{1, n, int64_t(cpr) * CH, 9};
+    return launch_pk(k_in, k_out, p_in, p_out, rows, tail, key_bytes, pay, xf, false, 0u, st, false, nullptr, &c);
+  }
+  return 0;
 }
 
 unsigned long long pksort_fallback_rows(bool reset) {

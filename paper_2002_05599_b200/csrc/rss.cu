@@ -1003,6 +1003,11 @@ int launch_rss(const nsg_spec& sp, const void* k_in, void* k_out, const void* p_
                int64_t n, int key_bytes, int pay, int mode, int layout, const Xform& xf, cudaStream_t st,
                const uint32_t* seg_ids = nullptr, const uint32_t* seg_off = nullptr,
                const uint32_t* seg_count = nullptr, uint32_t* seg_overflow = nullptr) {
+  // keys-only / UNIQUE rows of 513 .. midsort_cap items: the output is the
+  // unique sorted order -- packed-sorter chunks + merge-path passes (bigsort.cu)
+  if (sp.kind == NSG_KIND_RSS && layout == LAYOUT_SOA && !seg_ids && (pay == 0 || mode == MODE_UNIQUE) && n > 512 &&
+      n <= midsort_cap(key_bytes, pay) && !env_flag_set("NSG_RSS_FAITHFUL"))
+    return launch_midsort_rows(k_in, k_out, p_in, p_out, rows, n, key_bytes, pay, xf, st);
   if (n > 1024 && !seg_ids) {
     // keys-only / UNIQUE rows: the output is the unique sorted order -- CTA
     // sorter (bigsort.cu); the reference's tie order (REF mode with payloads,

@@ -72,8 +72,12 @@ typedef struct {
  * (netsort_core.c:498-527).  `rows` is a DEVICE pointer to m*n packed
  * {uint64 key; uint64 ref} items (items.py:14), 16-byte aligned, sorted in
  * place row by row.  kind NETWORK: n in 2..16 (n < 2 is a no-op, else -2);
- * kind RSS: any n (the reference's tie order, replayed draw for draw; above
- * 1024 items in global memory); kind INSERTION: stable by key, any n. */
+ * kind RSS: any n, the reference's tie order: rows of 17..512 items whose
+ * keys are all distinct (one sorted order) are sorted by the packed warp
+ * kernel, rows with equal keys are replayed draw for draw from a device list
+ * (a small stream-ordered allocation per call); other sizes are replayed draw
+ * for draw directly (above 1024 items in global memory); kind INSERTION:
+ * stable by key, any n. */
 int nsg_run_sorter_many(const nsg_spec* sp, void* rows, int64_t m, int64_t n, void* stream);
 
 /* Same with HOST rows (pinned memory overlaps copies with sorting). */
@@ -82,10 +86,12 @@ int nsg_run_sorter_many_host(const nsg_spec* sp, void* rows, int64_t m, int64_t 
 /* Typed SoA batch: `rows` rows of n keys (key_dtype) and optional payloads
  * (payload_dtype), row-major, device pointers, 16-byte aligned.  Out-of-place
  * or in-place (out == in).  Network kinds: n 1..16.  RSS, MERGE and INSERTION
- * kinds: any n (above 1024 items a stream-ordered scratch may be allocated:
- * keys-only / UNIQUE rows take a CTA sorter, REF-mode payload order the
- * reference recursion replayed in global memory).  MERGE requires UNIQUE
- * with a payload. */
+ * kinds: any n.  Keys-only / UNIQUE rows: 17..512 items the packed warp
+ * kernel, 513..80 KiB/item-bytes items its 512-item chunks plus merge-path
+ * passes in shared memory, longer ones a CTA sorter (a stream-ordered scratch
+ * may be allocated above its shared-memory capacity).  REF-mode payload
+ * order (RSS kind): as nsg_run_sorter_many.  MERGE requires UNIQUE with a
+ * payload. */
 int nsg_sort_rows(const nsg_spec* sp, const void* keys_in, void* keys_out, const void* pay_in, void* pay_out,
                   int64_t rows, int64_t n, void* stream);
 

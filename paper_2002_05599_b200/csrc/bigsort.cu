@@ -35,7 +35,13 @@ namespace {
 
 constexpr int kBigThreads = 1024;
 constexpr int kBigSmemBudget = 128 * 1024;
-constexpr int kMergePer = 8;  // outputs per thread per merge step
+#ifndef NSG_MERGE_PER
+#define NSG_MERGE_PER 8
+#endif
+#ifndef NSG_MID_STAGE_LAST
+#define NSG_MID_STAGE_LAST 1  // last merge pass into shared memory, then one coalesced copy out
+#endif
+constexpr int kMergePer = NSG_MERGE_PER;  // outputs per thread per merge step
 constexpr int kWarpV = 8;               // items per lane of a warp-register chunk
 constexpr int kWarpChunk = 32 * kWarpV;  // 256 items
 
@@ -424,12 +430,19 @@ __global__ void __launch_bounds__(T) rowmerge_kernel(const MidParams prm) {
     const U* sk = ak;
     const P* sp = ap;
     for (int w = kMidRun; w < n; w <<= 1) {
-      const bool last = 2 * w >= n;
+      const bool last = !NSG_MID_STAGE_LAST && 2 * w >= n;
       U* dk = last ? gk : (sk == ak ? bk : ak);
       P* dp = last ? gp : (sk == ak ? bp : ap);
       mid_pass<U, P>(sk, sp, dk, dp, n, w, prm.xf);
       sk = dk;
       sp = dp;
+    }
+    if constexpr (NSG_MID_STAGE_LAST) {  // (a thread's 8 merged outputs are 64 contiguous bytes: poor store coalescing)
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        gk[i] = sk[i];
+        if constexpr (HAS_P) gp[i] = sp[i];
+      }
+      __syncthreads();
     }
   }
 }
@@ -512,7 +525,7 @@ int launch_midsort_rows(const void* k_in, void* k_out, const void* p_in, void* p
   if (int rc = launch_pksort_chunks(k_in, k_out, p_in, p_out, rows, n, key_bytes, pay, xf, st)) return rc;
   const int pb = pay == 0 ? 0 : pay == 1 ? 4 : 8;
   const size_t kreg = (size_t(n) * key_bytes + 15) / 16 * 16, preg = (size_t(n) * pb + 15) / 16 * 16;
-  const bool two = n > 2 * kMidRun;  // more than one pass: a second buffer
+  const bool two = NSG_MID_STAGE_LAST || n > 2 * kMidRun;  // more than one pass (or a staged last pass): a second buffer
   const size_t smem = (kreg + preg) * (two ? 2 : 1);
   const bool big = n > 2048;
   const int threads = big ? kMidThreadsBig : kMidThreads;

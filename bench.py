@@ -118,9 +118,9 @@ class Cell:
         # staged by TMA (mirrors csrc/capi.cu dispatch: nettma_covers, netbulk.cu nb_choice)
         if self.kb == 8 and self.n == 16 and self.pb == 4:
             return f"nettma n=16 {fam} {kt} {pay} SoA UNIQUE"
-        if self.kb == 8 and self.pb in (0, 4) and self.n % 2 and 5 <= self.n <= 15 and self.n != 7:
+        if self.kb == 8 and self.pb in (0, 4) and self.n % 2 and 5 <= self.n <= 15:
             d = 0 if self.family == "best" else 1
-            bulk = (self.n in (5, 11, 13) or (self.n == 15 and d == 0)) if self.pb == 0 else \
+            bulk = (self.n in (5, 7, 11, 13) or (self.n == 15 and d == 0)) if self.pb == 0 else \
                 (self.n in (9, 11) or (self.n == 13 and d == 0) or self.n == 15)
             if bulk:
                 return f"netbulk n={self.n} {fam} {kt} {pay} SoA UNIQUE"

@@ -198,7 +198,8 @@ NbLaunch nb_mode(int mode) {
 // measured per shape (u64 keys; tools/nb_variants.py): 0 = the cp.async tile
 // kernel of net_sort.cuh stays faster, 1 = configuration A, 2 = B, 3 = C
 constexpr int nb_choice(int n, int dag, int pay) {
-  if (pay == 0) return n == 5 || (n == 13 && dag == 1) ? 3 : (n == 11 || n == 13 || (n == 15 && dag == 0)) ? 1 : 0;
+  if (pay == 0)
+    return n == 7 ? 2 : n == 5 || (n == 13 && dag == 1) ? 3 : (n == 11 || n == 13 || (n == 15 && dag == 0)) ? 1 : 0;
   if (n == 9 || n == 11) return 1;
   if ((n == 13 && dag == 0) || n == 15) return 2;
   return 0;
@@ -235,6 +236,7 @@ NbLaunch nb_dag(int dag, int pay, int mode) {
 NbLaunch nb_lookup(int n, int dag, int pay, int mode) {
   switch (n) {
     case 5: return nb_dag<5>(dag, pay, mode);
+    case 7: return nb_dag<7>(dag, pay, mode);
     case 9: return nb_dag<9>(dag, pay, mode);
     case 11: return nb_dag<11>(dag, pay, mode);
     case 13: return nb_dag<13>(dag, pay, mode);
@@ -248,7 +250,7 @@ NbLaunch nb_lookup(int n, int dag, int pay, int mode) {
 // u64 keys (+ u32 payload), SoA, the odd widths where the bulk-staged kernel
 // measured faster than the cp.async tile pipeline
 bool netbulk_covers(int n, int dag, int key_bytes, int pay) {
-  return key_bytes == 8 && (pay == 0 || pay == 1) && (n & 1) && n >= 5 && n <= 15 && n != 7 &&
+  return key_bytes == 8 && (pay == 0 || pay == 1) && (n & 1) && n >= 5 && n <= 15 &&
          (nb_force() != 0 || nb_choice(n, dag ? 1 : 0, pay) != 0);
 }
 

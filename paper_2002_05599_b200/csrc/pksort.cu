@@ -54,6 +54,7 @@ namespace {
 #endif
 
 __device__ unsigned long long g_pk_fallback_rows;  // diagnostics: rows re-sorted exactly
+__device__ unsigned long long g_pk_retry_groups;   // diagnostics: groups packed a second time (robust packing)
 
 struct PkParams {
   const void* k_in;
@@ -347,8 +348,9 @@ struct PhaseBitonic {
 template <class U, class P, int LOGNR, int E>
 struct PkPad {
   static constexpr int R = 32 * E >> LOGNR, L = (1 << LOGNR) / E;
-  static constexpr bool value = NSG_PK_PAD_MINR > 0 && R >= NSG_PK_PAD_MINR && sizeof(U) == 8 &&
-                                (IsNoPay<P>::value || sizeof(P) == 8) && L >= 2;
+  // (the pad of L elements keeps every row 16-byte aligned in both regions)
+  static constexpr bool value = NSG_PK_PAD_MINR > 0 && R >= NSG_PK_PAD_MINR && (L * sizeof(U)) % 16 == 0 &&
+                                (IsNoPay<P>::value || (L * PayBytes<P>::value) % 16 == 0);
 };
 #ifndef NSG_RSS_STRATIFIED
 #define NSG_RSS_STRATIFIED 1  // one sample per stratum of n/L columns
@@ -509,6 +511,98 @@ struct PhaseRss {
   }
 };
 
+// Second attempt for a group whose cheap packing degenerated (out of line:
+// the first attempt's code stays as it was).  The common-prefix window fails
+// when the keys straddle a high power of two with a small spread --
+// sign-extended small integers around zero: the first differing bit is the
+// sign, the next ~50 bits are all ones or all zeros, and the kept window sees
+// the sign only.  Pack the distance to the row's minimum in the ordered space
+// instead, sort, gather, and check again; returns the rows still out of order.
+template <class U, class P, int LOGNR, int E, bool FULL, class PH, int ST>
+__device__ __noinline__ unsigned pk_robust_group(U* rk, P* rp, uint32_t* pr, const PhaseCtx pc, const Xform xf,
+                                                 int rin) {
+  constexpr bool HAS_P = !IsNoPay<P>::value;
+  constexpr int NR = 1 << LOGNR, L = NR / E, LOGL = pk_ilog2(L), R = 32 * E / NR;
+  const int ll = pc.ll, rl = pc.rl;
+  const bool rowv = pc.rowv;
+  const U M = U(xf.sign_or ^ xf.kdesc);
+  auto kord = [&](U v) -> U { return xf.flt ? to_ord<U>(v, xf) : U(v ^ M); };
+  uint32_t pk[E];
+  {
+    U x[E];
+    U mn = U(~U(0));
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+      x[r] = kord(rk[(ll + L * r) * ST]);
+      if (FULL || r < rl) mn = x[r] < mn ? x[r] : mn;
+    }
+#pragma unroll
+    for (int m = 1; m < L; m <<= 1) {
+      const U o = shfl_xor_t<U>(mn, m);
+      mn = o < mn ? o : mn;
+    }
+    U acc = U(0);
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+      x[r] = U(x[r] - mn);
+      if (FULL || r < rl) acc |= x[r];
+    }
+#pragma unroll
+    for (int m = 1; m < L; m <<= 1) acc |= shfl_xor_t<U>(acc, m);
+    const int cp = acc ? clz_t(acc) : 0;
+    const int c2 = cp > 32 ? cp - 32 : 0;
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+      const uint32_t w = (top32c(x[r], cp, c2) & ~uint32_t(NR - 1)) | uint32_t(ll + L * r);
+      pk[r] = (FULL || r < rl) ? w : 0xffffffffu;
+    }
+  }
+  PH::sort(pk, pc);
+#pragma unroll
+  for (int r = 0; r < E; ++r) pr[ll * (E + 1) + r] = pk[r];
+  __syncwarp();
+  U ok[E];
+  P op[E];
+#pragma unroll
+  for (int r = 0; r < E; ++r) {
+    if (FULL || r < rl) {
+      const int q = ll + L * r;
+      const uint32_t idx = pr[L <= E ? q + (L * r) / E : q + q / E] & uint32_t(NR - 1);
+      ok[r] = rk[idx * ST];
+      if constexpr (HAS_P) op[r] = rp[idx * ST];
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < E; ++r) {
+    if (FULL || r < rl) {
+      rk[(ll + L * r) * ST] = ok[r];
+      if constexpr (HAS_P) rp[(ll + L * r) * ST] = op[r];
+    }
+  }
+  __syncwarp();
+  bool bad = false;
+#pragma unroll
+  for (int r = 0; r < E; ++r) {
+    const int q = ll + L * r;
+    const int qp = q - (q > 0 ? 1 : 0);
+    P a{}, bq{};
+    if constexpr (HAS_P) {
+      a = P(rp[qp * ST] ^ P(xf.pdesc));
+      bq = P(op[r] ^ P(xf.pdesc));
+    }
+    bad |= (FULL || r < rl) && item_lt<U, P>(kord(ok[r]), bq, kord(rk[qp * ST]), a);
+  }
+  const unsigned bm = __ballot_sync(0xffffffffu, bad && rowv);
+  unsigned bad_rows = 0u;
+#pragma unroll
+  for (int gg = 0; gg < R; ++gg) {
+    if ((bm >> (gg * L)) & (L == 32 ? 0xffffffffu : ((1u << L) - 1u))) bad_rows |= 1u << gg;
+  }
+  (void)rin;
+  return bad_rows;
+}
+
 // FULL: n == NR (no padding slots) -- the validity tests drop out; rows past
 // the end of the batch in the last group are sorted as garbage, never stored.
 template <class U, class P, int LOGNR, int E, bool FULL, class PH, bool PAD = false, bool AOS = false>
@@ -644,6 +738,7 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
     U* rk = fk + g * rs * ST;   // item i of the row: key rk[i * ST], payload rp[i * ST]
     P* rp = fp + g * rs * ST;
     const int rl = FULL ? E : rowv ? (n - ll + L - 1) >> LOGL : 0;  // valid r of this lane
+    unsigned bad_rows = 0u;
     uint32_t pk[E];
     if (!xf.flt) {
       // integer keys: ord(x) = x ^ M.  The common prefix of x ^ first is the
@@ -748,13 +843,14 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
     // ---- 5. rows with packed ties: full (key, payload) order check of every
     //         sorted neighbour pair in the staged output; failures re-sorted
     //         exactly (rare: distinct keys agreeing on every kept bit) ---------
-    unsigned bad_rows = forced & ((rin >= 32 ? 0u : (1u << rin)) - 1u);
+    bad_rows = forced & ((rin >= 32 ? 0u : (1u << rin)) - 1u);
+    unsigned badk_rows = 0u;  // rows with a KEY order violation (what a better packing can fix)
     if (tied) {
       // branch-free: every lane loads its E predecessors back to back (the
       // loads stay inside the buffer for every r; position 0 compares with
       // itself) and the validity masks are applied to the predicate
       const U M = U(xf.sign_or ^ xf.kdesc);
-      bool bad = false;
+      bool bad = false, badk = false;
       auto check = [&](auto kord) {
 #pragma unroll
         for (int r = 0; r < E; ++r) {
@@ -766,9 +862,12 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
             a = P(rp[qp * ST] ^ P(xf.pdesc));
             bq = P(op[r] ^ P(xf.pdesc));
           }
-          const bool lt = item_lt<U, P>(kord(ok[r]), bq, kord(pk_), a);
+          const U kc = kord(ok[r]), kp = kord(pk_);
+          const bool lt = item_lt<U, P>(kc, bq, kp, a);
           bad |= (FULL || r < rl) && lt;
+          if constexpr (HAS_P) badk |= (FULL || r < rl) && key_lt(kc, kp);
         }
+        if constexpr (!HAS_P) badk = bad;
       };
       // REF mode: a key-order violation OR an equal neighbour key (position 0
       // excepted: it compares with itself) sends the row to the draw-for-draw
@@ -798,9 +897,11 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
       }
       bad = bad && rowv;
       const unsigned bm = __ballot_sync(0xffffffffu, bad);
+      const unsigned bmk = __ballot_sync(0xffffffffu, badk && rowv);
 #pragma unroll
       for (int gg = 0; gg < R; ++gg) {
         if ((bm >> (gg * L)) & (L == 32 ? 0xffffffffu : ((1u << L) - 1u))) bad_rows |= 1u << gg;
+        if ((bmk >> (gg * L)) & (L == 32 ? 0xffffffffu : ((1u << L) - 1u))) badk_rows |= 1u << gg;
       }
       if constexpr (HAS_P) {
         if (ref && bad_rows) {
@@ -822,9 +923,22 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
             }
           }
           bad_rows = 0u;
+          badk_rows = 0u;
           __syncwarp();
         }
       }
+    }
+    // distinct keys of some row agreed on every kept bit and came out
+    // misordered: the whole group once more with the robust packing (cold,
+    // out of line); rows that still fail are re-sorted exactly below
+    // (merge phase only: the call costs the RSS phase's kernel 6-10 % on every
+    // input -- 1.52 -> 1.61 ms at n = 256 -- so its rare misordered rows go
+    // straight to the exact re-sort)
+    if (PH::SCRATCH == 0 && badk_rows != 0u) {
+      if (lane == 0) atomicAdd(&g_pk_retry_groups, 1ull);
+      __syncwarp();
+      const PhaseCtx pc{lane, g, ll, n, rl, rowv, scratch, spos, kk};
+      bad_rows = pk_robust_group<U, P, LOGNR, E, FULL, PH, ST>(rk, rp, pr, pc, xf, rin);
     }
 
     while (bad_rows) {

@@ -111,3 +111,23 @@ def test_merge_path_sentinel_ties(n, kdt, torch):
             ek, ep = oracle.typed_sort_rows(keys, pay, descending=desc, unique=True, kind="rss")
             k, p = batch.sort_rows(_t(torch, keys), _t(torch, pay), kind="merge", descending=desc, tie="unique")
             assert np.array_equal(k.cpu().numpy(), ek) and np.array_equal(p.cpu().numpy(), ep), (n, desc)
+
+
+@pytest.mark.parametrize("n", [32, 100, 256, 512])
+@pytest.mark.parametrize("kind", ["merge", "rss"])
+def test_sign_extended_small_keys(n, kind, torch):
+    """int64 keys of small magnitude and both signs: in the ordered space they
+    straddle 2^63, so the common-prefix window of the packed words sees the
+    sign only.  The merge phase packs the group a second time (distance to the
+    row minimum), the RSS phase re-sorts the rows exactly: same output."""
+    from paper_2002_05599_b200 import batch
+    from paper_2002_05599_b200._lib import lib
+    rng = np.random.default_rng(n)
+    keys = rng.integers(-1000, 1000, size=(4000, n), dtype=np.int64)
+    keys[::9] = rng.integers(-2**40, 2**40, size=keys[::9].shape, dtype=np.int64)
+    pay = rng.integers(0, 2**32, size=keys.shape, dtype=np.uint64).astype(np.uint32)
+    k, _ = batch.sort_rows(_t(torch, keys), kind=kind)
+    assert np.array_equal(k.cpu().numpy(), np.sort(keys, axis=1))
+    ek, ep = oracle.typed_sort_rows(keys, pay, unique=True, kind="rss")
+    k, p = batch.sort_rows(_t(torch, keys), _t(torch, pay), kind=kind, tie="unique")
+    assert np.array_equal(k.cpu().numpy(), ek) and np.array_equal(p.cpu().numpy().view(np.uint32), ep)

@@ -29,8 +29,11 @@ FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--
 def _units() -> list:
     """(object name, source, extra defines)"""
     units = [("net_n%02d.o" % n, CSRC / "net_sort_inst.cu", ["-DNSG_N=%d" % n]) for n in range(0, 17)]
-    for name in ("capi", "misc", "rss", "pksort", "bigsort", "netbulk", "nettma", "rssbig", "segments", "wmerge", "verify", "lane"):
+    for name in ("capi", "misc", "rss", "bigsort", "netbulk", "nettma", "rssbig", "segments", "wmerge", "verify", "lane"):
         units.append((name + ".o", CSRC / (name + ".cu"), []))
+    # the packed sorter's kernel instantiations build as three units in parallel (see pksort.cu)
+    for part in (1, 2, 3):
+        units.append(("pksort_p%d.o" % part, CSRC / "pksort.cu", ["-DNSG_PK_PART=%d" % part]))
     return units
 
 

@@ -53,8 +53,17 @@ namespace {
 #define NSG_PK_RING_BYTES 16384  // staging ring per warp: loads in flight ~ (ring - 2 buffers)
 #endif
 
+// This file is compiled as three translation units (build.py: -DNSG_PK_PART=1,
+// 2, 3; 0 or undefined = everything in one) so the kernel instantiations
+// build in parallel: part 1 holds the launchers, the u64 keys-only kernels
+// and the AoS ones; part 2 the u64 keys with payloads; part 3 the u32 keys.
+#ifndef NSG_PK_PART
+#define NSG_PK_PART 0
+#endif
+#if NSG_PK_PART <= 1
 __device__ unsigned long long g_pk_fallback_rows;  // diagnostics: rows re-sorted exactly
 __device__ unsigned long long g_pk_retry_groups;   // diagnostics: groups packed a second time (robust packing)
+#endif
 
 struct PkParams {
   const void* k_in;
@@ -81,6 +90,8 @@ struct PkParams {
   int cpr;
   int64_t outer_stride;
   int64_t first_off;
+  unsigned long long* fallback_ctr;  // diagnostics counters (device symbols of part 1)
+  unsigned long long* retry_ctr;
 };
 
 __host__ __device__ constexpr int pk_ilog2(int x) { return x <= 1 ? 0 : 1 + pk_ilog2(x >> 1); }
@@ -935,7 +946,7 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
     // input -- 1.52 -> 1.61 ms at n = 256 -- so its rare misordered rows go
     // straight to the exact re-sort)
     if (PH::SCRATCH == 0 && badk_rows != 0u) {
-      if (lane == 0) atomicAdd(&g_pk_retry_groups, 1ull);
+      if (lane == 0) atomicAdd(prm.retry_ctr, 1ull);
       __syncwarp();
       const PhaseCtx pc{lane, g, ll, n, rl, rowv, scratch, spos, kk};
       bad_rows = pk_robust_group<U, P, LOGNR, E, FULL, PH, ST>(rk, rp, pr, pc, xf, rin);
@@ -944,7 +955,7 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
     while (bad_rows) {
       const int gi = __ffs(int(bad_rows)) - 1;
       bad_rows &= bad_rows - 1;
-      if (lane == 0) atomicAdd(&g_pk_fallback_rows, 1ull);
+      if (lane == 0) atomicAdd(prm.fallback_ctr, 1ull);
       pk_exact_row<U, P, (NR > 256 ? 16 : 8)>(fk + gi * rs * ST, fp + gi * rs * ST, n, xf, lane, ST);
     }
 
@@ -1018,6 +1029,18 @@ const void* pk_fn(int lognr, bool full, bool rss, int* smem) {
   }
 }
 
+}  // namespace
+
+// kernel tables of the three parts (external linkage: part 1 calls all of them)
+const void* pk_pick_u64_keys(int lognr, bool full, bool rss, int* smem);
+const void* pk_pick_u64_pay(int pay, int lognr, bool full, bool rss, int* smem);
+const void* pk_pick_u32(int pay, int lognr, bool full, bool rss, int* smem);
+const void* pk_pick_aos(int lognr, bool full, int* smem);
+
+#if NSG_PK_PART == 0 || NSG_PK_PART == 1
+const void* pk_pick_u64_keys(int lognr, bool full, bool rss, int* smem) {
+  return pk_fn<uint64_t, NoPay>(lognr, full, rss, smem);
+}
 // reference items (AoS, u64 key + u64 ref): RSS phase up to 256 items, merge phase for 257..512
 const void* pk_pick_aos(int lognr, bool full, int* smem) {
   switch (lognr) {
@@ -1029,19 +1052,27 @@ const void* pk_pick_aos(int lognr, bool full, int* smem) {
     default: return nullptr;
   }
 }
-
-const void* pk_pick(int kb, int pay, int lognr, bool full, bool rss, int* smem) {
-  if (kb == 4) {
-    if (pay == 0) return pk_fn<uint32_t, NoPay>(lognr, full, rss, smem);
-    if (pay == 1) return pk_fn<uint32_t, uint32_t>(lognr, full, rss, smem);
-    return pk_fn<uint32_t, uint64_t>(lognr, full, rss, smem);
-  }
-  if (pay == 0) return pk_fn<uint64_t, NoPay>(lognr, full, rss, smem);
+#endif
+#if NSG_PK_PART == 0 || NSG_PK_PART == 2
+const void* pk_pick_u64_pay(int pay, int lognr, bool full, bool rss, int* smem) {
   if (pay == 1) return pk_fn<uint64_t, uint32_t>(lognr, full, rss, smem);
   return pk_fn<uint64_t, uint64_t>(lognr, full, rss, smem);
 }
+#endif
+#if NSG_PK_PART == 0 || NSG_PK_PART == 3
+const void* pk_pick_u32(int pay, int lognr, bool full, bool rss, int* smem) {
+  if (pay == 0) return pk_fn<uint32_t, NoPay>(lognr, full, rss, smem);
+  if (pay == 1) return pk_fn<uint32_t, uint32_t>(lognr, full, rss, smem);
+  return pk_fn<uint32_t, uint64_t>(lognr, full, rss, smem);
+}
+#endif
 
-}  // namespace
+#if NSG_PK_PART <= 1
+static const void* pk_pick(int kb, int pay, int lognr, bool full, bool rss, int* smem) {
+  if (kb == 4) return pk_pick_u32(pay, lognr, full, rss, smem);
+  if (pay == 0) return pk_pick_u64_keys(lognr, full, rss, smem);
+  return pk_pick_u64_pay(pay, lognr, full, rss, smem);
+}
 
 bool pksort_covers(int64_t n) { return n >= 17 && n <= 512; }       // merge phase
 bool pksort_rss_covers(int64_t n) { return n >= 17 && n <= 256; }   // RSS phase (8-word blocks, 32 lanes)
@@ -1074,7 +1105,11 @@ static int launch_pk(const void* k_in, void* k_out, const void* p_in, void* p_ou
   }
   PkParams prm{k_in, k_out, p_in, p_out, rows, int(n), bulk ? 1 : 0, 1u, 0xffffffffu, seed == 0 ? 1u : seed, xf,
                defer ? 1 : 0, defer ? defer->count : nullptr, defer ? defer->ids : nullptr, defer ? defer->cap : 0,
-               chunks ? chunks->cpr : 0, chunks ? chunks->outer_stride : 0, chunks ? chunks->first_off : 0};
+               chunks ? chunks->cpr : 0, chunks ? chunks->outer_stride : 0, chunks ? chunks->first_off : 0,
+               nullptr, nullptr};
+  if (cudaGetSymbolAddress(reinterpret_cast<void**>(&prm.fallback_ctr), g_pk_fallback_rows) != cudaSuccess ||
+      cudaGetSymbolAddress(reinterpret_cast<void**>(&prm.retry_ctr), g_pk_retry_groups) != cudaSuccess)
+    return fail(NSG_ERR_CUDA, "pksort: counter symbols");
   int sms = 0, occ = 0;
   constexpr int threads = NSG_PK_WARPS * 32;
   if (int rc = kernel_residency(fn, threads, smem, &occ, &sms)) return rc;
@@ -1138,5 +1173,6 @@ unsigned long long pksort_fallback_rows(bool reset) {
   }
   return v;
 }
+#endif  // NSG_PK_PART <= 1
 
 }  // namespace nsg

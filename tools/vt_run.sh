@@ -2,6 +2,8 @@
 # On the GPU box: run a probe against the product ("base") and variant builds
 # (tools/unit_variants.py).  Usage: PROBE="python tools/cfg3_probe.py ..." bash tools/vt_run.sh base v1 v2 ...
 # Prints the probe's output lines prefixed with the variant name.
+# Needs the product's objects and the variants' on the box: take
+# paper_2002_05599_b200/build/ and variants/ out of .gpurunignore while tuning.
 PROBE=${PROBE:-python tools/workloads.py --which cfg4}
 for v in "$@"; do
   if [ "$v" = base ]; then

@@ -363,6 +363,9 @@ struct PkPad {
   static constexpr bool value = NSG_PK_PAD_MINR > 0 && R >= NSG_PK_PAD_MINR && (L * sizeof(U)) % 16 == 0 &&
                                 (IsNoPay<P>::value || (L * PayBytes<P>::value) % 16 == 0);
 };
+#ifndef NSG_RSS_RETRY
+#define NSG_RSS_RETRY 1  // RSS phase: second attempt with the robust packing (see the kernel)
+#endif
 #ifndef NSG_RSS_STRATIFIED
 #define NSG_RSS_STRATIFIED 1  // one sample per stratum of n/L columns
 #endif
@@ -749,9 +752,45 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
     U* rk = fk + g * rs * ST;   // item i of the row: key rk[i * ST], payload rp[i * ST]
     P* rp = fp + g * rs * ST;
     const int rl = FULL ? E : rowv ? (n - ll + L - 1) >> LOGL : 0;  // valid r of this lane
-    unsigned bad_rows = 0u;
+    unsigned bad_rows = 0u, merge_badk = 0u;
+    // RSS phase: a group whose cheap packing degenerated runs once more through
+    // this loop with the robust packing (inline: +2 % on every input, where
+    // the out-of-line second attempt of the merge phase, pk_robust_group, cost
+    // this kernel 6-10 %).  Merge phase: one trip, the loop folds away.
+    constexpr bool kLoopRetry = PH::SCRATCH != 0 && NSG_RSS_RETRY != 0;
+    for (int attempt = 0;; ++attempt) {
     uint32_t pk[E];
-    if (!xf.flt) {
+    if (kLoopRetry && attempt == 1) {
+      const U M = U(xf.sign_or ^ xf.kdesc);  // (see pk_robust_group)
+      U x[E];
+      U mn = U(~U(0));
+#pragma unroll
+      for (int r = 0; r < E; ++r) {
+        const U raw = rk[(ll + L * r) * ST];
+        x[r] = xf.flt ? to_ord<U>(raw, xf) : U(raw ^ M);
+        if (FULL || r < rl) mn = x[r] < mn ? x[r] : mn;
+      }
+#pragma unroll
+      for (int m = 1; m < L; m <<= 1) {
+        const U o = shfl_xor_t<U>(mn, m);
+        mn = o < mn ? o : mn;
+      }
+      U acc = U(0);
+#pragma unroll
+      for (int r = 0; r < E; ++r) {
+        x[r] = U(x[r] - mn);
+        if (FULL || r < rl) acc |= x[r];
+      }
+#pragma unroll
+      for (int m = 1; m < L; m <<= 1) acc |= shfl_xor_t<U>(acc, m);
+      const int cp = acc ? clz_t(acc) : 0;
+      const int c2 = cp > 32 ? cp - 32 : 0;
+#pragma unroll
+      for (int r = 0; r < E; ++r) {
+        const uint32_t w = (top32c(x[r], cp, c2) & ~uint32_t(NR - 1)) | uint32_t(ll + L * r);
+        pk[r] = (FULL || r < rl) ? w : 0xffffffffu;
+      }
+    } else if (!xf.flt) {
       // integer keys: ord(x) = x ^ M.  The common prefix of x ^ first is the
       // same in both spaces, and the shifted top word of ord(x) is the shifted
       // top word of x xor that of M, so the transform costs one XOR per row.
@@ -939,17 +978,22 @@ __global__ void __launch_bounds__(NSG_PK_WARPS * 32) pksort_kernel(const PkParam
         }
       }
     }
+    if (!(kLoopRetry && attempt == 0 && badk_rows != 0u)) {
+      if (!kLoopRetry) merge_badk = badk_rows;
+      break;
+    }
+    if (lane == 0) atomicAdd(prm.retry_ctr, 1ull);
+    __syncwarp();
+    }  // attempts
     // distinct keys of some row agreed on every kept bit and came out
-    // misordered: the whole group once more with the robust packing (cold,
-    // out of line); rows that still fail are re-sorted exactly below
-    // (merge phase only: the call costs the RSS phase's kernel 6-10 % on every
-    // input -- 1.52 -> 1.61 ms at n = 256 -- so its rare misordered rows go
-    // straight to the exact re-sort)
-    if (PH::SCRATCH == 0 && badk_rows != 0u) {
+    // misordered: the whole group once more with the robust packing (merge
+    // phase: cold, out of line); rows that still fail are re-sorted exactly below
+    if (PH::SCRATCH == 0 && merge_badk != 0u) {
       if (lane == 0) atomicAdd(prm.retry_ctr, 1ull);
       __syncwarp();
       const PhaseCtx pc{lane, g, ll, n, rl, rowv, scratch, spos, kk};
-      bad_rows = pk_robust_group<U, P, LOGNR, E, FULL, PH, ST>(rk, rp, pr, pc, xf, rin);
+      uint32_t* pr2 = pa + g * S;
+      bad_rows = pk_robust_group<U, P, LOGNR, E, FULL, PH, ST>(rk, rp, pr2, pc, xf, rin);
     }
 
     while (bad_rows) {

@@ -120,6 +120,32 @@ def main():
         assert np.array_equal(gk.cpu().numpy().view(np.uint32), ek.view(np.uint32))
         assert np.array_equal(gp.cpu().numpy(), ep)
         checks += 1
+    # midsort (513..10240 items: packed chunks + merge-path passes), ragged tails,
+    # and the robust second packing (small keys of both signs)
+    for n in (513, 1000, 1024, 3000, 10240):
+        keys = rng.integers(-2**63, 2**63 - 1, size=(37, n), dtype=np.int64)
+        keys[::3] = rng.integers(-500, 500, size=keys[::3].shape)
+        pay = rng.integers(0, 2**32, size=(37, n), dtype=np.uint64).astype(np.uint32)
+        for kind in ("merge", "rss"):
+            k, _ = batch.sort_rows(t(keys), kind=kind)
+            assert np.array_equal(k.cpu().numpy(), np.sort(keys, axis=1)), (kind, n)
+            checks += 1
+        if n <= 6000:
+            k, p = batch.sort_rows(t(keys), t(pay), kind="merge", tie="unique")
+            ek, ep = oracle.typed_sort_rows(keys, pay, unique=True, kind="rss")
+            assert np.array_equal(k.cpu().numpy(), ek) and np.array_equal(p.cpu().numpy().view(np.uint32), ep), n
+            checks += 1
+    # REF items through the packed kernel + deferred rows (AoS staging)
+    for n in (40, 256, 400):
+        items = np.empty((500, n), dtype=oracle.ITEM)
+        items["key"] = rng.integers(0, 2**64, size=(500, n), dtype=np.uint64)
+        items["key"][::5] %= np.uint64(4)
+        items["ref"] = np.arange(500 * n, dtype=np.uint64).reshape(500, n)
+        exp = items.copy()
+        oracle.run_items(exp, kind="rss", rss_cfg="332")
+        backend.run_sorter_many(registry.spec_rss("332"), items)
+        assert np.array_equal(items, exp), n
+        checks += 1
     torch.cuda.synchronize()
     print(f"sanitize probe ok ({checks} checks)")
 

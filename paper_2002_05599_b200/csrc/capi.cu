@@ -200,6 +200,18 @@ int nsg_version(void) { return 100; }
 
 uint32_t nsg_lcg_next(uint32_t seed) { return uint32_t((uint64_t(seed) * 48271u) % 2147483647u); }
 
+// An RSS spec on rows no longer than its base-case threshold IS the base case
+// (ns_rss_rec, netsort_core.c:325-391: n <= threshold -> ns_small_base): with a
+// network base that is the spec's family network of exactly n items, which the
+// network kernels run at the memory roofline (DAG-exact in REF mode).  With an
+// insertion base the same holds when the output order is unique.
+static bool rss_is_network(const nsg_spec* sp, int64_t n, bool unique_order) {
+  if (sp->kind != NSG_KIND_RSS || n < 2 || n > 16 || n > sp->rss_threshold) return false;
+  if (sp->rss_oversampling < 1 || sp->rss_oversampling > 16 || sp->rss_threshold < 2) return false;  // (rejected later)
+  if (sp->base_kind == 0) return sp->rss_threshold <= 16;
+  return unique_order;
+}
+
 int nsg_sort_rows(const nsg_spec* sp, const void* keys_in, void* keys_out, const void* pay_in, void* pay_out,
                   int64_t rows, int64_t n, void* stream) {
   g_err.clear();
@@ -214,7 +226,7 @@ int nsg_sort_rows(const nsg_spec* sp, const void* keys_in, void* keys_out, const
     return fail(NSG_ERR_SPEC, "device buffers must be 16-byte aligned");
   if (rows == 0 || n == 0) return 0;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (sp->kind == NSG_KIND_NETWORK) {
+  if (sp->kind == NSG_KIND_NETWORK || rss_is_network(sp, n, !has_p || sp->tie_mode == NSG_TIE_UNIQUE)) {
     if (n > 16) return fail(NSG_ERR_SPEC, "network sorters cover 2..16 items, got %lld", (long long)n);
     if (nettma_covers(int(n), kb, sp->payload_dtype) && !env_flag("NSG_NET_TILE_ONLY")) {
       const int rc = launch_nettma(dag_of(*sp), sp->payload_dtype, sp->tie_mode, keys_in, keys_out, pay_in, pay_out,
@@ -267,7 +279,7 @@ int nsg_run_sorter_many(const nsg_spec* sp, void* rows, int64_t m, int64_t n, vo
   if (!aligned16(rows)) return fail(NSG_ERR_SPEC, "item rows must be 16-byte aligned");
   if (m == 0 || n == 0) return 0;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (sp->kind == NSG_KIND_NETWORK) {
+  if (sp->kind == NSG_KIND_NETWORK || rss_is_network(sp, n, false)) {
     if (n < 2) return 0;  // ns_run_sorter: n < 2 -> 0 (netsort_core.c:502-503)
     if (n > 16) return fail(NSG_ERR_SPEC, "network sorters cover 2..16 items, got %lld", (long long)n);
     NetParams prm{rows, rows, nullptr, nullptr, m, Xform{}};

@@ -31,8 +31,8 @@ def main():
         for dist in ("distinct", "dup1pct", "few16"):
             keys = torch.randint(-2**63, 2**63 - 1, (a.rows, n), dtype=torch.int64, device=dev, generator=g)
             if dist == "few16":
-                keys = keys[:, :16][torch.arange(a.rows, device=dev)[:, None],
-                                    torch.randint(0, 16, (a.rows, n), device=dev, generator=g)]
+                vals = torch.randint(-2**63, 2**63 - 1, (a.rows, 16), dtype=torch.int64, device=dev, generator=g)
+                keys = torch.gather(vals, 1, torch.randint(0, 16, (a.rows, n), device=dev, generator=g))
             elif dist == "dup1pct":  # one row in a hundred carries a duplicated key
                 keys[::100, 1] = keys[::100, 0]
             items = torch.empty((a.rows, n, 2), dtype=torch.int64, device=dev)

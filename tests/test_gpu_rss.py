@@ -259,3 +259,28 @@ def test_packed_sorters_lane_copy_fallback(torch, monkeypatch):
         oracle.run_items(exp, kind="rss", rss_cfg="332")
         backend.run_sorter_many(registry.spec_rss("332"), items)
         assert np.array_equal(items, exp), n
+
+
+@pytest.mark.parametrize("n", [2, 5, 11, 16])
+def test_rss_rows_within_base_threshold(n, torch):
+    """An RSS spec on rows of <= threshold items is its base case: the family's
+    n-item network (C-ABI routes it to the network kernels).  Typed rows, REF
+    and UNIQUE, and reference items with an insertion base (draw-for-draw kernel)."""
+    from paper_2002_05599_b200 import backend, batch, registry
+    rng = np.random.default_rng(70 + n)
+    keys = rng.integers(0, 6, size=(3001, n)).astype(np.int64) - 3
+    pay = rng.integers(0, 2**31, size=(3001, n)).astype(np.uint32)
+    for tie in ("unique", "ref"):
+        for desc in (False, True):
+            ek, ep = oracle.typed_sort_rows(keys, pay, descending=desc, unique=tie == "unique", kind="rss")
+            gk, gp = batch.sort_rows(torch.from_numpy(keys).cuda(),
+                                     torch.from_numpy(pay.view(np.int32)).cuda().view(torch.uint32),
+                                     kind="rss", descending=desc, tie=tie)
+            assert np.array_equal(gk.cpu().numpy(), ek), (tie, desc)
+            assert np.array_equal(gp.cpu().numpy().view(np.uint32), ep), (tie, desc)
+    for cfg, base, fam, kb in (("332", "SN BN-L 4CmS", "bn-l", "net"), ("341", "IS Def", "best", "ins")):
+        items = _items(keys.view(np.uint64), np.arange(keys.size, dtype=np.uint64).reshape(keys.shape))
+        exp = items.copy()
+        oracle.run_items(exp, kind="rss", family=fam, rss_cfg=cfg, base=kb)
+        backend.run_sorter_many(registry.spec_rss(cfg, base), items)
+        assert np.array_equal(items, exp), (cfg, base)
